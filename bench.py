@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the fused ITLUMM hot path (one step = itlumm_amm over one batch of rows).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--algo auto|simt|tc]
+  python bench.py --impl reference ...     # the CPU oracle, timed as it stands (reference arm)
+
+N > 1 runs under torchrun (one process per GPU, NCCL): rank 0 fits the layer once and
+broadcasts its parameters; every rank then processes its own N rows (weak scaling, no
+collective in the data path).  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOAD_DESC = {
+    "cfg1": "BASELINE configs[0]: MNIST-shaped final layer, N=1000 D=784 M=10 C=16 (no ReLU)",
+    "cfg2": "BASELINE configs[1]: MNIST-shaped hidden layer, N=60000 D=784 M=512 C=32, seeded permutation, ReLU",
+    "cfg3_c64": "BASELINE configs[2]: CIFAR-shaped layer, N=50000 D=3072 M=1024 C=64",
+    "cfg3_c128": "BASELINE configs[2]: CIFAR-shaped layer, N=50000 D=3072 M=1024 C=128",
+    "cfg5": "BASELINE configs[4]: FFN-shaped stress case, N=262144 D=4096 M=4096 C=256, bf16 input",
+}
+METRIC = "fused ITLUMM rows/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def alg_bytes(w: dict, n: int) -> int:
+    """A split columns + output + LUT = N*(4C*s_A + 4M) + 16CM per launch."""
+    s_a = 2 if w["dtype"] == "bf16" else 4
+    return n * (4 * w["C"] * s_a + 4 * w["M"]) + 16 * w["C"] * w["M"]
+
+
+def ncu_traffic(workload: str, algo: str):
+    """dram read+write bytes per launch from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(f"{workload}:{algo}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.out = None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits", "-lms", "50"],
+                                     stdout=self.out, stderr=subprocess.DEVNULL)
+        time.sleep(0.3)
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        self.out.flush()
+        with open(self.out.name) as f:
+            lines = [l.strip() for l in f if l.strip()]
+        os.unlink(self.out.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 10:
+                continue
+            try:
+                sm.append(float(parts[2]))
+                mx = float(parts[3])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[6:10]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2207_05808_b200 import Plan, fit_layer
+    from paper_2207_05808_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.workload]
+    n = cfg["N"] if args.rows is None else args.rows
+    relu = cfg["relu"]
+    bf16 = cfg["dtype"] == "bf16"
+
+    # offline fit on rank 0 (host), broadcast once over NCCL, plan on every rank
+    params = None
+    if rank == 0:
+        w0 = synth.workload(args.workload, n_rows=0)
+        params = fit_layer(w0["A_train"], w0["B"], w0["C"], w0["perm"], w0["bias"], a_is_bf16=bf16)
+    if world > 1:
+        params = pdist.broadcast_params(params, dev)
+    plan = Plan(params, device=local, algo=args.algo)
+
+    # this rank's rows (weak scaling: rank r owns rows [r*n, (r+1)*n) of the seeded stream)
+    r0, r1 = pdist.weak_rows(n, rank)
+    A_host = synth.rows(cfg["dist"], cfg["cfg"], 0, r0, r1, cfg["D"])
+    A_t = torch.from_numpy(A_host.view(np.int16) if bf16 else A_host)
+    A_pin = A_t.pin_memory()
+    nbuf = 2
+    A_dev = [A_pin.to(dev) for _ in range(nbuf)]
+    if bf16:
+        A_dev = [a.view(torch.bfloat16) for a in A_dev]
+        A_pin = A_pin.view(torch.bfloat16)
+    out_dev = [torch.empty((n, cfg["M"]), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        plan.amm(A_dev[i % nbuf], out=out_dev[i % nbuf], relu=relu)
+        return plan.last_launch_count
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        launches += step(i)
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if world > 1:
+        total_ms = pdist.max_over_ranks(total_ms, dev)
+        launch_ms = pdist.max_over_ranks(launch_ms, dev)
+    ms_per_step = total_ms / args.steps
+    rows_per_s = n * world / (ms_per_step * 1e-3)
+
+    # end to end through the host-buffer C-ABI call (H2D + kernel + D2H inside the region)
+    out_pin = torch.empty((n, cfg["M"]), dtype=torch.float32).pin_memory()
+    k_e2e = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        plan.amm_host(A_pin, out=out_pin, relu=relu)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        plan.amm_host(A_pin, out=out_pin, relu=relu)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / k_e2e
+    if world > 1:
+        e2e_s = pdist.max_over_ranks(e2e_s, dev)
+        dist.barrier()
+    e2e = {"value": n * world / e2e_s, "unit": "rows/s",
+           "h2d_bytes_per_step": int(A_host.nbytes), "d2h_bytes_per_step": int(n * cfg["M"] * 4),
+           "api": "itlumm_amm_host (pinned host buffers, chunked H2D/kernel/D2H)", "steps": k_e2e}
+
+    peak, peak_src = peaks()
+    ab = alg_bytes(cfg, n)
+    achieved = ab / (launch_ms * 1e-3) / 1e9
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(args.workload, params, n, budget_s=args.cpu_budget)
+        line = {
+            "metric": METRIC, "value": rows_per_s, "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded stand-in for the dataset, DESIGN.md input recipe)",
+            "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
+                       "rows_per_gpu": n, "global_rows": n * world, "D": cfg["D"], "C": cfg["C"],
+                       "M": cfg["M"], "input": ("bf16" if bf16 else "f32") + " row-major",
+                       "epilogue": "relu" if relu else "none", "algo": args.algo,
+                       "parallelism": f"rows sharded dp{world}",
+                       "l2": f"inputs larger than L2 (A {A_host.nbytes / 2**20:.0f} MiB/step) and "
+                             f"{nbuf} rotating A/out buffer sets",
+                       "compute": "uint8 LUT, exact int32 accumulate, fp32 compare + fmaf dequant"},
+            "output_elems_per_s": rows_per_s * cfg["M"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload, args.algo),
+                         "alg_bytes_per_launch": ab, "launch_ms": launch_ms,
+                         "peak_source": peak_src, "kernel": "itlumm_amm (fused)"},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+# --------------------------------------------------------------------------------- oracle
+def _oracle_rows_per_s(params, A, relu, dtype, nthreads):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.amm(params, A, relu=relu, dtype=dtype, nthreads=nthreads)
+    return A.shape[0] / (time.perf_counter() - t0)
+
+
+def cpu_baseline(workload: str, params: dict, n: int, budget_s: float = 15.0):
+    """The oracle (plain C, never tuned) on the host cores, on a bounded sample of the same
+    workload (fitted parameters shared); ~budget_s seconds of work."""
+    cfg = synth.CONFIGS[workload]
+    cores = os.cpu_count() or 1
+    dtype = "bf16" if cfg["dtype"] == "bf16" else "f32"
+    probe = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"])
+    rate = _oracle_rows_per_s(params, probe, cfg["relu"], dtype, cores)
+    n_s = int(max(512, min(n, rate * budget_s)))
+    A = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, n_s, cfg["D"])
+    v = _oracle_rows_per_s(params, A, cfg["relu"], dtype, cores)
+    return {"value": v, "unit": "rows/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n_s} of the {n} rows of {workload} (rank 0), full encode+accumulate+dequant"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as it stands on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    from oracle import fit as ofit
+    cfg = synth.CONFIGS[args.workload]
+    n = cfg["N"] if args.rows is None else args.rows
+    w0 = synth.workload(args.workload, n_rows=0)
+    bf16 = cfg["dtype"] == "bf16"
+    params = ofit.fit(w0["A_train"], w0["B"], w0["C"], w0["perm"], w0["bias"], a_is_bf16=bf16)
+    dtype = "bf16" if bf16 else "f32"
+    cores = os.cpu_count() or 1
+    probe = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"])
+    rate = _oracle_rows_per_s(params, probe, cfg["relu"], dtype, cores)
+    per_step = int(max(1, min(n, rate * args.ref_budget / max(1, args.steps + args.warmup))))
+    A = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, per_step, cfg["D"])
+    for _ in range(args.warmup):
+        oracle.amm(params, A, relu=cfg["relu"], dtype=dtype, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.amm(params, A, relu=cfg["relu"], dtype=dtype, nthreads=cores)
+    dt = time.perf_counter() - t0
+    v = per_step * args.steps / dt
+    sample = f"first {per_step} of the {n} rows of {args.workload} per step"
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
+                       "rows_per_step": per_step, "D": cfg["D"], "C": cfg["C"], "M": cfg["M"]},
+            "cpu_baseline": {"value": v, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--rows", type=int, default=None, help="override rows per GPU (default: config N)")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/* itlumm.h — C ABI of the B200-native ITLUMM / MADDNESS inference hot path.
+ *
+ * The problem: approximate sigma(A.B) for a FIXED weight
+ * matrix B that has been folded offline into a lookup table h(B) = quantise(P.B), with a learned
+ * encoder g(A).  Per activation row a:
+ *   a1  permutation / partition: a'[i] = a[perm[i]], chunk c = a'[b_c .. b_{c+1})
+ *   a2  encode: depth-4 balanced regression tree, K = 16, "exactly 4 comparisons":
+ *         node = 0; for t = 0..3: node = 2*node + (chunk_c[split_dim[c][t]] > thr[c][2^t-1+node])
+ *         code_c = node
+ *   a3  lookup-accumulate: acc[m] = sum_c lut[c][code_c][m], uint8 entries summed EXACTLY in
+ *         32-bit integers ("rounded 8-bit summation": reading R7 in DESIGN.md)
+ *   a4  dequantise (+ReLU): y[m] = fmaf(scale[m], (float)acc[m], offtot[m]) with
+ *         offtot[m] = (float)((double)C*(double)offset[m] + (double)bias[m])     (reading R8);
+ *         ReLU: y > 0 ? y : +0                                                     (R9)
+ * K = 16 is fixed.  Every entry point is asynchronous on `stream` unless stated otherwise.
+ *
+ * Conventions for every call
+ *   - Status codes: ITLUMM_OK on success; otherwise the call has no effect on outputs and
+ *     itlumm_last_error() returns a thread-local message naming the failed check.
+ *   - Device pointers are caller-owned CUDA device allocations on the plan's device; host
+ *     pointers are caller-owned host memory.  The library never frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - N = 0 returns ITLUMM_OK without launching anything.
+ *   - There is NO CPU fallback: a kernel that cannot run returns ITLUMM_EUNSUPPORTED/ECUDA.
+ *   - Asynchronous device faults surface at the caller's next synchronisation.
+ *   - Concurrent calls on one plan from several host threads/streams are safe: the plan is
+ *     immutable after creation ("pure and reentrant"), except itlumm_amm_host, which
+ *     uses plan-owned staging buffers and serialises itself with a mutex.
+ */
+#ifndef ITLUMM_H
+#define ITLUMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ITLUMM_ABI_VERSION 1
+
+typedef enum {
+  ITLUMM_OK = 0,
+  ITLUMM_EINVAL = 1,        /* bad argument: null pointer, bad size/stride, invalid parameters */
+  ITLUMM_ESHAPE = 2,        /* call inconsistent with the plan ("shape mismatch") */
+  ITLUMM_EUNSUPPORTED = 3,  /* shape/dtype/alignment the selected kernel cannot take          */
+  ITLUMM_ECUDA = 4,         /* CUDA launch/config/runtime failure (cudaGetErrorString in msg) */
+  ITLUMM_ENOMEM = 5         /* device or host allocation failure                             */
+} itlumm_status;
+
+typedef enum { ITLUMM_F32 = 0, ITLUMM_BF16 = 1 } itlumm_dtype;            /* element type of A */
+typedef enum { ITLUMM_EPI_NONE = 0, ITLUMM_EPI_RELU = 1 } itlumm_epilogue;  /* sigma    */
+
+/* Kernel family used by itlumm_amm / itlumm_lut_accumulate.
+ *   AUTO  : library choice (documented in DESIGN.md "kernel selection")
+ *   SIMT  : CUDA-core shared-memory LUT kernels (any shape within the limits below)
+ *   TC    : tcgen05 one-hot x LUT int8 tensor-core kernel (G.T with G the one-hot encoding,
+ *           P:89; exact integer products) — EUNSUPPORTED where its tiling does not apply.
+ * Both families produce bit-identical results. */
+typedef enum { ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2 } itlumm_algo;
+
+typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */
+
+/* Fitted layer parameters.  HOST pointers, read only during itlumm_plan_create (copied). */
+typedef struct {
+  int32_t D;                 /* input dim (columns of A)                                     */
+  int32_t C;                 /* codebooks, 1 <= C <= D                                      */
+  int32_t M;                 /* output dim (columns of B / of the result)                    */
+  const int32_t* perm;       /* [D] bijection, a'[i] = a[perm[i]]; NULL = identity (R11)     */
+  const int32_t* boundaries; /* [C+1], 0 = b_0 < b_1 < ... < b_C = D; NULL = equal chunks,
+                                larger first (R12: first D mod C chunks get one extra dim)  */
+  const int32_t* split_dim;  /* [C][4] subspace-local split dim per level, 0 <= sd < d_c     */
+  const float* thresholds;   /* [C][15] heap order: level t, node n at (2^t - 1) + n; no NaN
+                                (+-inf allowed)                                  */
+  const uint8_t* lut;        /* [C][16][M] quantised table q (16*C*M bytes)            */
+  const float* scale;        /* [M] per-output scale, finite                                 */
+  const float* offset;       /* [M] per-output offset lo_m (min of column m of T), finite    */
+  const float* bias;         /* [M] or NULL (= 0), finite                                     */
+} itlumm_params;
+
+/* Validate `p`, fold the permutation into absolute gather columns
+ * col[c][t] = perm[b_c + split_dim[c][t]], compute offtot, lay the LUT out for the kernels and
+ * copy everything to `cuda_device`.  Blocking.  On success *out owns the device copies.
+ * Errors: EINVAL (null required pointer; D, C or M < 1; C > D; perm not a bijection;
+ * boundaries not strictly increasing from 0 to D; split_dim outside [0, d_c); NaN threshold;
+ * non-finite scale/offset/bias; bad device), ENOMEM, ECUDA. */
+itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_device, itlumm_plan* out);
+
+/* Free the plan's device memory (synchronises the plan's device).  NULL is a no-op. */
+itlumm_status itlumm_plan_destroy(itlumm_plan plan);
+
+/* Select the kernel family (default AUTO).  Not thread-safe against concurrent launches. */
+itlumm_status itlumm_plan_set_algo(itlumm_plan plan, itlumm_algo algo);
+
+/* Query plan dims: any out-pointer may be NULL.  lut_bytes = 16*C*M. */
+itlumm_status itlumm_plan_info(itlumm_plan plan, int32_t* D, int32_t* C, int32_t* M,
+                               int64_t* lut_bytes);
+
+/* a1 + a2.  A: device, N rows x lda elements of `dtype`, row-major, lda >= D; only the 4C
+ * split columns of each row are read.  codes: device, N x ldc bytes, ldc >= ceil(C/2);
+ * row r byte i holds code 2i in its low nibble and code 2i+1 in its high nibble (R14; an odd
+ * C leaves the last high nibble 0).  Errors: EINVAL (null, N < 0, lda < D, ldc < ceil(C/2),
+ * bad dtype), ECUDA. */
+itlumm_status itlumm_encode(itlumm_plan plan, const void* A, itlumm_dtype dtype, int64_t lda,
+                            int64_t N, uint8_t* codes, int64_t ldc, void* stream);
+
+/* a3 (+ a4).  codes as produced by itlumm_encode.  acc: device int32 [N][ldacc] (ldacc >= M)
+ * or NULL; out: device fp32 [N][ldo] (ldo >= M) or NULL; at least one must be non-NULL.
+ * `epi` applies to `out` only.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+itlumm_status itlumm_lut_accumulate(itlumm_plan plan, const uint8_t* codes, int64_t ldc,
+                                    int64_t N, int32_t* acc, int64_t ldacc, float* out,
+                                    int64_t ldo, itlumm_epilogue epi, void* stream);
+
+/* Fused a1..a4: one kernel, codes never reach HBM.  A as in itlumm_encode, out device fp32
+ * [N][ldo], ldo >= M.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+itlumm_status itlumm_amm(itlumm_plan plan, const void* A, itlumm_dtype dtype, int64_t lda,
+                         int64_t N, float* out, int64_t ldo, itlumm_epilogue epi, void* stream);
+
+/* Fused a1..a4 on HOST buffers (end-to-end API).  A_host: N x lda elements (pinned memory is
+ * fastest; pageable works), out_host: N x ldo fp32.  Rows are streamed through plan-owned
+ * device staging buffers in chunks with H2D copy / kernel / D2H copy overlapped across two
+ * internal streams.  Ordered after prior work on `stream`; BLOCKING: returns when out_host is
+ * written.  Staging is allocated on first use (ENOMEM possible) and kept by the plan.
+ * Errors: as itlumm_amm, plus ENOMEM. */
+itlumm_status itlumm_amm_host(itlumm_plan plan, const void* A_host, itlumm_dtype dtype,
+                              int64_t lda, int64_t N, float* out_host, int64_t ldo,
+                              itlumm_epilogue epi, void* stream);
+
+/* Number of kernel launches the last successful launching call on this thread made. */
+int32_t itlumm_last_launch_count(void);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* itlumm_last_error(void);
+
+/* ITLUMM_ABI_VERSION of the loaded library. */
+int32_t itlumm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ITLUMM_H */

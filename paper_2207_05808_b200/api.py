@@ -1,0 +1,130 @@
+"""Thin Python binding over the C ABI (argument marshalling only).
+
+torch tensors supply device memory (``data_ptr()``) and the stream
+(``torch.cuda.current_stream().cuda_stream``); every step of the hot path runs in the CUDA
+kernels of libitlumm.so.  Names follow include/itlumm.h."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype_code(t):
+    if t.dtype == torch.float32:
+        return _lib.F32
+    if t.dtype in (torch.bfloat16, torch.int16, torch.uint16):
+        return _lib.BF16
+    raise TypeError(f"A must be float32 or bfloat16, got {t.dtype}")
+
+
+class Plan:
+    """An immutable ITLUMM layer on one GPU (itlumm_plan)."""
+
+    def __init__(self, params: dict, device: int = 0, algo: str = "auto"):
+        self._lib = _lib.load()
+        D, C, M = int(params["D"]), int(params["C"]), int(params["M"])
+        keep = dict(
+            perm=np.ascontiguousarray(params["perm"], np.int32) if params.get("perm") is not None else None,
+            boundaries=(np.ascontiguousarray(params["boundaries"], np.int32)
+                        if params.get("boundaries") is not None else None),
+            split_dim=np.ascontiguousarray(params["split_dim"], np.int32),
+            thresholds=np.ascontiguousarray(params["thresholds"], np.float32),
+            lut=np.ascontiguousarray(params["lut"], np.uint8),
+            scale=np.ascontiguousarray(params["scale"], np.float32),
+            offset=np.ascontiguousarray(params["offset"], np.float32),
+            bias=np.ascontiguousarray(params["bias"], np.float32) if params.get("bias") is not None else None,
+        )
+        p = _lib.Params(D, C, M, *[_np_ptr(keep[k]) for k in
+                                   ("perm", "boundaries", "split_dim", "thresholds", "lut", "scale",
+                                    "offset", "bias")])
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.itlumm_plan_create(ctypes.byref(p), int(device), ctypes.byref(h)))
+        self._h = h
+        self.D, self.C, self.M, self.device = D, C, M, int(device)
+        self.set_algo(algo)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.itlumm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_algo(self, algo: str):
+        _lib.check(self._lib.itlumm_plan_set_algo(self._h, _lib.ALGO[algo]))
+        self.algo = algo
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self._lib.itlumm_last_launch_count())
+
+    # ------------------------------------------------------------------ device-pointer calls
+    def encode(self, A, codes=None, stream=None):
+        """a1+a2: A [N, lda>=D] fp32/bf16 on the plan's device -> packed codes [N, ceil(C/2)] u8."""
+        N = A.shape[0]
+        if codes is None:
+            codes = torch.empty((N, (self.C + 1) // 2), dtype=torch.uint8, device=A.device)
+        _lib.check(self._lib.itlumm_encode(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
+                                           A.stride(0), N, ctypes.c_void_p(codes.data_ptr()),
+                                           codes.stride(0), _stream(stream)))
+        return codes
+
+    def lut_accumulate(self, codes, out=None, acc=None, relu=False, want_out=True, stream=None):
+        """a3(+a4): packed codes -> fp32 out [N, M] (and/or int32 acc [N, M])."""
+        N = codes.shape[0]
+        if out is None and want_out:
+            out = torch.empty((N, self.M), dtype=torch.float32, device=codes.device)
+        _lib.check(self._lib.itlumm_lut_accumulate(
+            self._h, ctypes.c_void_p(codes.data_ptr()), codes.stride(0), N,
+            ctypes.c_void_p(acc.data_ptr()) if acc is not None else None,
+            acc.stride(0) if acc is not None else self.M,
+            ctypes.c_void_p(out.data_ptr()) if out is not None else None,
+            out.stride(0) if out is not None else self.M,
+            _lib.EPI_RELU if relu else _lib.EPI_NONE, _stream(stream)))
+        return out, acc
+
+    def amm(self, A, out=None, relu=False, stream=None):
+        """Fused a1..a4: A [N, lda>=D] -> out [N, M] fp32 (codes never reach HBM)."""
+        N = A.shape[0]
+        if out is None:
+            out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
+        _lib.check(self._lib.itlumm_amm(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
+                                        A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
+                                        out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
+                                        _stream(stream)))
+        return out
+
+    # ------------------------------------------------------------------ host-buffer call
+    def amm_host(self, A, out=None, relu=False, stream=None):
+        """End-to-end: HOST rows (torch CPU tensor, pinned is fastest) -> HOST out [N, M] fp32.
+        Blocking; H2D / kernel / D2H are pipelined inside the library."""
+        N = A.shape[0]
+        if out is None:
+            out = torch.empty((N, self.M), dtype=torch.float32, pin_memory=A.is_pinned())
+        _lib.check(self._lib.itlumm_amm_host(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
+                                             A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
+                                             out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
+                                             _stream(stream)))
+        return out

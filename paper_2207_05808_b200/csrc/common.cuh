@@ -1,0 +1,71 @@
+// common.cuh — device helpers shared by the ITLUMM kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "itlumm kernels are written for sm_100a (B200) only"
+#endif
+
+namespace itlumm {
+
+constexpr int kLevels = 4;   // "exactly 4 comparisons"
+constexpr int kK = 16;       // prototypes per codebook
+
+// Device-side view of a plan (passed by value to kernels).
+struct DevPlan {
+  const int32_t* cols;    // [C][4] absolute gather column: perm[b_c + split_dim[c][t]] (a1 folded)
+  const float* thr_t;     // [15][C] thresholds, heap index major (lanes = codebooks -> no bank conflicts)
+  const uint8_t* lut;     // [C][16][Mp] uint8 LUT, Mp = roundup(M,16), zero padded
+  const float* scale;     // [Mp]
+  const float* offtot;    // [Mp] (float)((double)C*lo + bias)
+  int D, C, M, Mp;
+};
+
+template <typename T> struct InTraits;
+template <> struct InTraits<float> {
+  static __device__ __forceinline__ float load(const float* p) { return __ldg(p); }
+};
+// bf16 is carried as raw uint16 bit patterns; widening to fp32 is exact (reading R13).
+template <> struct InTraits<uint16_t> {
+  static __device__ __forceinline__ float load(const uint16_t* p) {
+    return __uint_as_float(static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(p))) << 16);
+  }
+};
+
+// One depth-4 tree walk (a2): node <- 2*node + (v_t > thr[2^t-1+node]); NaN compares false.
+__device__ __forceinline__ int tree_walk(const float v[4], const float* thr_t, int C, int c) {
+  int node = 0;
+#pragma unroll
+  for (int t = 0; t < kLevels; ++t) {
+    const float th = thr_t[((1 << t) - 1 + node) * C + c];
+    node = 2 * node + (v[t] > th ? 1 : 0);
+  }
+  return node;
+}
+
+// Named barriers (bar.sync / bar.arrive) for the producer/consumer ring.
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// 16-bit-lane SWAR widening of 4 uint8 LUT entries: even bytes / odd bytes (one PRMT each).
+__device__ __forceinline__ uint32_t even_bytes(uint32_t w) { return __byte_perm(w, 0u, 0x4240); }
+__device__ __forceinline__ uint32_t odd_bytes(uint32_t w) { return __byte_perm(w, 0u, 0x4341); }
+
+// acc += x issued as IMAD (x * one + acc) so that the adds run on the FMA pipe and leave the
+// ALU pipe to the PRMT widening; `one` is a runtime 1 the compiler cannot fold.
+__device__ __forceinline__ void add_fma_pipe(uint32_t& acc, uint32_t x, uint32_t one) {
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(x), "r"(one));
+}
+
+__device__ __forceinline__ float relu_pos0(float y) { return y > 0.0f ? y : 0.0f; }
+
+__device__ __forceinline__ void st_cs_f4(float* p, float a, float b, float c, float d) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
+}
+
+}  // namespace itlumm

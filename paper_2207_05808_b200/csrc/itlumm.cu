@@ -1,0 +1,453 @@
+// itlumm.cu — host library behind include/itlumm.h: plan validation, permutation folding,
+// parameter layout on the device, kernel selection and launches, the pipelined host API.
+// Every arithmetic step of the hot path runs in the kernels (simt.cuh, tc.cuh); the host only
+// validates, re-lays-out parameters once per plan, and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/itlumm.h"
+#include "common.cuh"
+#include "simt.cuh"
+#include "tc.cuh"
+
+using namespace itlumm;
+
+// ------------------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static thread_local int32_t g_launches = 0;
+
+static itlumm_status fail(itlumm_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(ITLUMM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------ plan
+struct SimtCfg {
+  int MS = 0, R = 0, S = 0, G = 0;
+  size_t smem_fused = 0, smem_codes = 0;
+  int grid_fused = 0, grid_codes = 0;
+};
+
+struct itlumm_plan_s {
+  int device = 0;
+  int D = 0, C = 0, M = 0, Mp = 0;
+  int num_sms = 0;
+  itlumm_algo algo = ITLUMM_ALGO_AUTO;
+  void* dmem = nullptr;  // one allocation holding every device parameter
+  DevPlan dp{};
+  SimtCfg simt{};
+  TcPlan tc{};
+  // host API staging
+  std::mutex host_mu;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  cudaEvent_t hev = nullptr;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+static bool finite_all(const float* v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+typedef void (*lut_kernel_t)(DevPlan, LutArgs);
+
+template <bool FUSED, typename T>
+static lut_kernel_t pick_lut_kernel(int MS) {
+  switch (MS) {
+    case 16: return k_lut<16, FUSED, T>;
+    case 32: return k_lut<32, FUSED, T>;
+    case 64: return k_lut<64, FUSED, T>;
+    case 128: return k_lut<128, FUSED, T>;
+    case 256: return k_lut<256, FUSED, T>;
+  }
+  return nullptr;
+}
+
+static itlumm_status set_smem(lut_kernel_t k, size_t smem) {
+  CUDA_TRY(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return ITLUMM_OK;
+}
+
+// Choose the SIMT tiling: the widest power-of-two M slice whose LUT stays resident in shared
+// memory, then the tile height and ring depth.
+static itlumm_status configure_simt(itlumm_plan_s* P) {
+  const int C = P->C;
+  const size_t budget = 200 * 1024;
+  int mp2 = 16;
+  while (mp2 < P->Mp && mp2 < 256) mp2 <<= 1;
+  const int C4 = (C + 3) & ~3;
+  for (int MS = mp2; MS >= 16; MS >>= 1) {
+    const int LPR = MS / 16;
+    int R = kConsumers / LPR;
+    int S = 4;
+    // offset ring <= 48 KB
+    while (R > 1 && (size_t)S * R * C4 * 4 > 48 * 1024) R >>= 1;
+    if (lut_smem_bytes(C, MS, R, S, true) <= budget) {
+      SimtCfg& s = P->simt;
+      s.MS = MS; s.R = R; s.S = S;
+      s.G = (P->Mp + MS - 1) / MS;
+      s.smem_fused = lut_smem_bytes(C, MS, R, S, true);
+      s.smem_codes = lut_smem_bytes(C, MS, R, S, false);
+      lut_kernel_t kf32 = pick_lut_kernel<true, float>(MS), kbf = pick_lut_kernel<true, uint16_t>(MS),
+                   kc = pick_lut_kernel<false, float>(MS);
+      itlumm_status st;
+      if ((st = set_smem(kf32, s.smem_fused)) != ITLUMM_OK) return st;
+      if ((st = set_smem(kbf, s.smem_fused)) != ITLUMM_OK) return st;
+      if ((st = set_smem(kc, s.smem_codes)) != ITLUMM_OK) return st;
+      int occ_f = 0, occ_c = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf32, kLutThreads, s.smem_fused));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, kLutThreads, s.smem_codes));
+      occ_f = std::max(occ_f, 1);
+      occ_c = std::max(occ_c, 1);
+      s.grid_fused = s.G * std::max(1, P->num_sms * occ_f / s.G);
+      s.grid_codes = s.G * std::max(1, P->num_sms * occ_c / s.G);
+      return ITLUMM_OK;
+    }
+  }
+  return ITLUMM_OK;  // simt.MS == 0: SIMT kernels unsupported for this C (C > ~780)
+}
+
+extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_device, itlumm_plan* out) {
+  g_err.clear();
+  if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!p) return fail(ITLUMM_EINVAL, "params is NULL");
+  const int D = p->D, C = p->C, M = p->M;
+  if (D < 1 || C < 1 || M < 1) return fail(ITLUMM_EINVAL, "D, C, M must be >= 1 (got %d, %d, %d)", D, C, M);
+  if (C > D) return fail(ITLUMM_EINVAL, "C (%d) > D (%d)", C, D);
+  if (!p->split_dim || !p->thresholds || !p->lut || !p->scale || !p->offset)
+    return fail(ITLUMM_EINVAL, "split_dim, thresholds, lut, scale and offset are required");
+  // a1: permutation and partition
+  std::vector<int32_t> perm(D), bnd(C + 1);
+  if (p->perm) {
+    std::vector<char> seen(D, 0);
+    for (int i = 0; i < D; ++i) {
+      const int v = p->perm[i];
+      if (v < 0 || v >= D || seen[v]) return fail(ITLUMM_EINVAL, "perm is not a bijection of [0, D) (perm[%d] = %d)", i, v);
+      seen[v] = 1;
+      perm[i] = v;
+    }
+  } else {
+    for (int i = 0; i < D; ++i) perm[i] = i;
+  }
+  if (p->boundaries) {
+    for (int c = 0; c <= C; ++c) bnd[c] = p->boundaries[c];
+    if (bnd[0] != 0 || bnd[C] != D) return fail(ITLUMM_EINVAL, "boundaries must start at 0 and end at D");
+    for (int c = 0; c < C; ++c)
+      if (bnd[c + 1] <= bnd[c]) return fail(ITLUMM_EINVAL, "boundaries not strictly increasing at %d", c);
+  } else {
+    const int q = D / C, r = D % C;  // reading R12: larger chunks first
+    bnd[0] = 0;
+    for (int c = 0; c < C; ++c) bnd[c + 1] = bnd[c] + q + (c < r ? 1 : 0);
+  }
+  std::vector<int32_t> cols(4 * (size_t)C);
+  for (int c = 0; c < C; ++c)
+    for (int t = 0; t < kLevels; ++t) {
+      const int sd = p->split_dim[c * 4 + t];
+      if (sd < 0 || sd >= bnd[c + 1] - bnd[c])
+        return fail(ITLUMM_EINVAL, "split_dim[%d][%d] = %d outside [0, %d)", c, t, sd, bnd[c + 1] - bnd[c]);
+      cols[c * 4 + t] = perm[bnd[c] + sd];   // folded gather column
+    }
+  for (int i = 0; i < C * 15; ++i)
+    if (std::isnan(p->thresholds[i])) return fail(ITLUMM_EINVAL, "threshold %d is NaN", i);
+  if (!finite_all(p->scale, M) || !finite_all(p->offset, M) || (p->bias && !finite_all(p->bias, M)))
+    return fail(ITLUMM_EINVAL, "scale/offset/bias must be finite");
+
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(ITLUMM_EINVAL, "bad cuda_device %d (have %d)", cuda_device, ndev);
+
+  itlumm_plan_s* P = new (std::nothrow) itlumm_plan_s();
+  if (!P) return fail(ITLUMM_ENOMEM, "host allocation failed");
+  P->device = cuda_device;
+  P->D = D; P->C = C; P->M = M; P->Mp = (M + 15) & ~15;
+  const int Mp = P->Mp;
+
+  // host images of the device parameters
+  std::vector<float> thr_t((size_t)15 * C);
+  for (int c = 0; c < C; ++c)
+    for (int h = 0; h < 15; ++h) thr_t[(size_t)h * C + c] = p->thresholds[c * 15 + h];
+  std::vector<uint8_t> lut((size_t)C * 16 * Mp, 0);
+  for (size_t r = 0; r < (size_t)C * 16; ++r) memcpy(&lut[r * Mp], p->lut + r * M, M);
+  std::vector<float> scale(Mp, 0.f), offtot(Mp, 0.f);
+  for (int m = 0; m < M; ++m) {
+    scale[m] = p->scale[m];
+    const double b = p->bias ? (double)p->bias[m] : 0.0;
+    offtot[m] = (float)((double)C * (double)p->offset[m] + b);   // reading R8
+  }
+  std::vector<uint8_t> qt;
+  tc_layout_host(C, M, p->lut, &P->tc, qt);
+
+  // one device allocation
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t o_cols = 0, o_thr = o_cols + al(cols.size() * 4), o_lut = o_thr + al(thr_t.size() * 4),
+               o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mp * 4), o_qt = o_ot + al((size_t)Mp * 4),
+               total = o_qt + al(qt.size());
+  int prev = 0;
+  cudaGetDevice(&prev);
+  auto cleanup = [&](itlumm_status st) {
+    if (P->dmem) cudaFree(P->dmem);
+    delete P;
+    cudaSetDevice(prev);
+    return st;
+  };
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e)));
+  cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  e = cudaMalloc(&P->dmem, total);
+  if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e)));
+  uint8_t* base = (uint8_t*)P->dmem;
+  struct { size_t off; const void* src; size_t n; } cp[] = {
+      {o_cols, cols.data(), cols.size() * 4}, {o_thr, thr_t.data(), thr_t.size() * 4},
+      {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mp * 4},
+      {o_ot, offtot.data(), (size_t)Mp * 4},  {o_qt, qt.data(), qt.size()}};
+  for (auto& c : cp) {
+    if (!c.n) continue;
+    e = cudaMemcpy(base + c.off, c.src, c.n, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e)));
+  }
+  P->dp.cols = (const int32_t*)(base + o_cols);
+  P->dp.thr_t = (const float*)(base + o_thr);
+  P->dp.lut = base + o_lut;
+  P->dp.scale = (const float*)(base + o_sc);
+  P->dp.offtot = (const float*)(base + o_ot);
+  P->dp.D = D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
+  P->tc.qt = qt.empty() ? nullptr : base + o_qt;
+  itlumm_status st = configure_simt(P);
+  if (st != ITLUMM_OK) return cleanup(st);
+  st = tc_configure(P->tc, P->num_sms);
+  if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
+  cudaSetDevice(prev);
+  *out = P;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
+  g_err.clear();
+  if (!P) return ITLUMM_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(P->device);
+  cudaDeviceSynchronize();
+  if (P->dmem) cudaFree(P->dmem);
+  if (P->stage) cudaFree(P->stage);
+  for (auto& s : P->hs)
+    if (s) cudaStreamDestroy(s);
+  if (P->hev) cudaEventDestroy(P->hev);
+  cudaSetDevice(prev);
+  delete P;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_set_algo(itlumm_plan P, itlumm_algo algo) {
+  g_err.clear();
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC)
+    return fail(ITLUMM_EINVAL, "bad algo %d", (int)algo);
+  P->algo = algo;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_info(itlumm_plan P, int32_t* D, int32_t* C, int32_t* M, int64_t* lut_bytes) {
+  g_err.clear();
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (D) *D = P->D;
+  if (C) *C = P->C;
+  if (M) *M = P->M;
+  if (lut_bytes) *lut_bytes = (int64_t)16 * P->C * P->M;
+  return ITLUMM_OK;
+}
+
+// ------------------------------------------------------------------------------ launches
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev); else prev = -1;
+  }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+static itlumm_status check_A(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N) {
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (N < 0) return fail(ITLUMM_EINVAL, "N < 0");
+  if (dtype != ITLUMM_F32 && dtype != ITLUMM_BF16) return fail(ITLUMM_EINVAL, "bad dtype %d", (int)dtype);
+  if (N > 0 && !A) return fail(ITLUMM_EINVAL, "A is NULL");
+  if (lda < P->D) return fail(ITLUMM_EINVAL, "lda (%lld) < D (%d)", (long long)lda, P->D);
+  return ITLUMM_OK;
+}
+
+static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda,
+                                   int64_t N, uint8_t* codes, int64_t ldc, cudaStream_t s) {
+  const int64_t nb = (P->C + 1) / 2;
+  const int64_t total = N * nb;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)P->num_sms * 32);
+  if (dtype == ITLUMM_F32)
+    k_encode<float><<<(unsigned)blocks, 256, 0, s>>>(P->dp, (const float*)A, lda, N, codes, ldc);
+  else
+    k_encode<uint16_t><<<(unsigned)blocks, 256, 0, s>>>(P->dp, (const uint16_t*)A, lda, N, codes, ldc);
+  CUDA_TRY(cudaGetLastError());
+  g_launches = 1;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda,
+                                       int64_t N, uint8_t* codes, int64_t ldc, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  itlumm_status st = check_A(P, A, dtype, lda, N);
+  if (st != ITLUMM_OK) return st;
+  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_EINVAL, "ldc (%lld) < ceil(C/2) (%d)", (long long)ldc, (P->C + 1) / 2);
+  if (N == 0) return ITLUMM_OK;
+  if (!codes) return fail(ITLUMM_EINVAL, "codes is NULL");
+  DeviceGuard dg(P->device);
+  return launch_encode(P, A, dtype, lda, N, codes, ldc, (cudaStream_t)stream);
+}
+
+static bool use_tc(itlumm_plan P) {
+  if (P->algo == ITLUMM_ALGO_SIMT) return false;
+  if (P->algo == ITLUMM_ALGO_TC) return true;
+  return tc_preferred(P->tc, P->simt.MS != 0);
+}
+
+static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm_dtype dtype, int64_t lda,
+                                const uint8_t* codes, int64_t ldc, int64_t N, int32_t* acc, int64_t ldacc,
+                                float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
+  if (use_tc(P)) {
+    if (!P->tc.ok) return fail(ITLUMM_EUNSUPPORTED, "tensor-core path unsupported for this plan: %s", P->tc.why);
+    TcArgs a{};
+    a.A = A; a.lda = lda; a.codes = codes; a.ldc = ldc; a.N = N; a.acc = acc; a.ldacc = ldacc;
+    a.out = out; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
+    itlumm_status st = tc_launch(P->tc, P->dp, fused, dtype == ITLUMM_BF16, a, s);
+    if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
+    g_launches = 1;
+    return ITLUMM_OK;
+  }
+  const SimtCfg& c = P->simt;
+  if (c.MS == 0) return fail(ITLUMM_EUNSUPPORTED, "SIMT LUT kernel: C = %d too large for a resident LUT slice", P->C);
+  LutArgs g{};
+  g.A = A; g.lda = lda; g.codes = codes; g.ldc = ldc; g.N = N;
+  g.acc = acc; g.ldacc = ldacc; g.out = out; g.ldo = ldo;
+  g.relu = epi == ITLUMM_EPI_RELU;
+  const bool out_al = !out || (((uintptr_t)out % 16) == 0 && ldo % 4 == 0);
+  const bool acc_al = !acc || (((uintptr_t)acc % 16) == 0 && ldacc % 4 == 0);
+  g.vec_out = out_al && acc_al;
+  g.R = c.R; g.S = c.S; g.G = c.G; g.one = 1u;
+  const int64_t ntiles = (N + c.R - 1) / c.R;
+  int grid = fused ? c.grid_fused : c.grid_codes;
+  const int64_t maxgrid = (int64_t)c.G * ntiles;
+  if (grid > maxgrid) grid = (int)maxgrid;
+  lut_kernel_t k = fused ? (dtype == ITLUMM_BF16 ? pick_lut_kernel<true, uint16_t>(c.MS)
+                                                 : pick_lut_kernel<true, float>(c.MS))
+                         : pick_lut_kernel<false, float>(c.MS);
+  k<<<grid, kLutThreads, fused ? c.smem_fused : c.smem_codes, s>>>(P->dp, g);
+  CUDA_TRY(cudaGetLastError());
+  g_launches = 1;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_lut_accumulate(itlumm_plan P, const uint8_t* codes, int64_t ldc, int64_t N,
+                                               int32_t* acc, int64_t ldacc, float* out, int64_t ldo,
+                                               itlumm_epilogue epi, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (N < 0) return fail(ITLUMM_EINVAL, "N < 0");
+  if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
+  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_EINVAL, "ldc (%lld) < ceil(C/2)", (long long)ldc);
+  if (acc && ldacc < P->M) return fail(ITLUMM_EINVAL, "ldacc < M");
+  if (out && ldo < P->M) return fail(ITLUMM_EINVAL, "ldo < M");
+  if (N == 0) return ITLUMM_OK;
+  if (!codes) return fail(ITLUMM_EINVAL, "codes is NULL");
+  if (!acc && !out) return fail(ITLUMM_EINVAL, "acc and out are both NULL");
+  DeviceGuard dg(P->device);
+  return launch_lut(P, false, nullptr, ITLUMM_F32, 0, codes, ldc, N, acc, ldacc, out, ldo, epi, (cudaStream_t)stream);
+}
+
+extern "C" itlumm_status itlumm_amm(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N,
+                                    float* out, int64_t ldo, itlumm_epilogue epi, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  itlumm_status st = check_A(P, A, dtype, lda, N);
+  if (st != ITLUMM_OK) return st;
+  if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
+  if (ldo < P->M) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
+  if (N == 0) return ITLUMM_OK;
+  if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  DeviceGuard dg(P->device);
+  return launch_lut(P, true, A, dtype, lda, nullptr, 0, N, nullptr, 0, out, ldo, epi, (cudaStream_t)stream);
+}
+
+extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlumm_dtype dtype, int64_t lda,
+                                         int64_t N, float* out_host, int64_t ldo, itlumm_epilogue epi,
+                                         void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  itlumm_status st = check_A(P, A_host, dtype, lda, N);
+  if (st != ITLUMM_OK) return st;
+  if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
+  if (ldo < P->M) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
+  if (N == 0) return ITLUMM_OK;
+  if (!out_host) return fail(ITLUMM_EINVAL, "out_host is NULL");
+  std::lock_guard<std::mutex> lk(P->host_mu);
+  DeviceGuard dg(P->device);
+  const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
+  const size_t row_in = (size_t)P->D * es, row_out = (size_t)P->M * 4;
+  // chunk of rows per pipeline stage: ~32 MB of input, at least 1024 rows
+  int64_t chunk = std::max<int64_t>(1024, (int64_t)((32u << 20) / row_in));
+  chunk = std::min<int64_t>(chunk, N);
+  const size_t in_b = ((size_t)chunk * row_in + 255) & ~(size_t)255, out_b = ((size_t)chunk * row_out + 255) & ~(size_t)255;
+  const size_t need = 2 * (in_b + out_b);
+  if (P->stage_bytes < need) {
+    if (P->stage) { cudaDeviceSynchronize(); cudaFree(P->stage); P->stage = nullptr; P->stage_bytes = 0; }
+    if (cudaMalloc(&P->stage, need) != cudaSuccess) return fail(ITLUMM_ENOMEM, "staging cudaMalloc(%zu)", need);
+    P->stage_bytes = need;
+  }
+  for (auto& s : P->hs)
+    if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (!P->hev) CUDA_TRY(cudaEventCreateWithFlags(&P->hev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(P->hev, (cudaStream_t)stream));
+  for (auto& s : P->hs) CUDA_TRY(cudaStreamWaitEvent(s, P->hev, 0));
+  int32_t launches = 0;
+  for (int64_t r0 = 0, i = 0; r0 < N; r0 += chunk, ++i) {
+    const int64_t rows = std::min<int64_t>(chunk, N - r0);
+    cudaStream_t s = P->hs[i & 1];
+    uint8_t* dA = (uint8_t*)P->stage + (i & 1) * (in_b + out_b);
+    float* dO = (float*)(dA + in_b);
+    CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, (const uint8_t*)A_host + (size_t)r0 * lda * es, (size_t)lda * es,
+                               row_in, rows, cudaMemcpyHostToDevice, s));
+    st = launch_lut(P, true, dA, dtype, P->D, nullptr, 0, rows, nullptr, 0, dO, P->M, epi, s);
+    if (st != ITLUMM_OK) return st;
+    launches += 1;
+    CUDA_TRY(cudaMemcpy2DAsync(out_host + (size_t)r0 * ldo, (size_t)ldo * 4, dO, row_out, row_out, rows,
+                               cudaMemcpyDeviceToHost, s));
+  }
+  for (auto& s : P->hs) CUDA_TRY(cudaStreamSynchronize(s));
+  g_launches = launches;
+  return ITLUMM_OK;
+}
+
+extern "C" int32_t itlumm_last_launch_count(void) { return g_launches; }
+extern "C" const char* itlumm_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t itlumm_abi_version(void) { return ITLUMM_ABI_VERSION; }

@@ -1,0 +1,113 @@
+"""Offline fit of an ITLUMM layer on the host (fit-time, NOT the hot path).
+
+The paper's contributions are all fit-time; the inference path (the CUDA library)
+consumes what this module produces: gather permutation + partition, depth-4 trees, and the
+uint8 LUT with per-output scale/offset.  The rules follow the same readings as the oracle
+(R3-R6, R12) but this is an independent, vectorised implementation; the test
+suite checks that both produce bit-identical parameters.
+
+Reductions are defined so that results are reproducible bit for bit: node means and node sums
+of squares are numpy reductions over the node's rows in ascending row order; the LUT is
+accumulated over subspace dims in ascending order (product rounded, then added).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+N_LEVELS = 4
+N_PROTO = 16
+
+
+def chunk_bounds(D: int, C: int) -> np.ndarray:
+    """C contiguous chunks of the permuted dims, sizes differing by <= 1, larger first (R12)."""
+    if C < 1 or C > D:
+        raise ValueError(f"need 1 <= C <= D, got C={C}, D={D}")
+    sizes = np.full(C, D // C, dtype=np.int64)
+    sizes[: D % C] += 1
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+
+
+def _segments(leaf: np.ndarray, n_nodes: int):
+    order = np.argsort(leaf, kind="stable")
+    cnt = np.bincount(leaf, minlength=n_nodes)
+    starts = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    return order, cnt, starts
+
+
+def _fit_subspace(X: np.ndarray):
+    """One tree (R3/R4) + leaf-mean prototypes (R5) for one subspace X (n x d, fp64)."""
+    n, d = X.shape
+    leaf = np.zeros(n, dtype=np.int64)
+    split = np.zeros(N_LEVELS, dtype=np.int32)
+    thr = np.zeros(2 ** N_LEVELS - 1, dtype=np.float64)
+    level_means = []
+    for t in range(N_LEVELS + 1):
+        nn = 2 ** t
+        order, cnt, starts = _segments(leaf, nn)
+        means = np.zeros((nn, d))
+        sse = np.zeros(d)
+        for node in range(nn):
+            if cnt[node]:
+                Xn = X[order[starts[node]:starts[node] + cnt[node]]]
+                means[node] = Xn.mean(axis=0)
+                if t < N_LEVELS:
+                    sse += ((Xn - means[node]) ** 2).sum(axis=0)
+        level_means.append((means, cnt))
+        if t == N_LEVELS:
+            break
+        j = int(np.argmax(sse))
+        split[t] = j
+        # lower median per node: sort rows by (node, value), take index (cnt-1)//2 of each segment
+        key = np.lexsort((X[:, j], leaf))
+        base = 2 ** t - 1
+        for node in range(nn):
+            h = base + node
+            if cnt[node]:
+                thr[h] = X[key[starts[node] + (cnt[node] - 1) // 2], j]
+            else:
+                thr[h] = thr[(h - 1) // 2]
+        leaf = 2 * leaf + (X[:, j] > thr[base + leaf]).astype(np.int64)
+    # prototypes: leaf mean, or the nearest non-empty ancestor's mean for an empty leaf
+    P = np.zeros((N_PROTO, d))
+    for k in range(N_PROTO):
+        for t in range(N_LEVELS, -1, -1):
+            means, cnt = level_means[t]
+            node = k >> (N_LEVELS - t)
+            if cnt[node]:
+                P[k] = means[node]
+                break
+    return split, thr, P
+
+
+def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | None = None,
+              bias: np.ndarray | None = None, a_is_bf16: bool = False) -> dict:
+    """Fit trees and the quantised LUT of one layer approximating A @ B (+ bias).
+
+    Returns the parameter dict consumed by :class:`paper_2207_05808_b200.Plan`."""
+    A = np.asarray(A_train)
+    if a_is_bf16:
+        A = (A.astype(np.uint32) << 16).view(np.float32)
+    A = A.astype(np.float32)
+    D = A.shape[1]
+    B = np.asarray(B, dtype=np.float64)
+    M = B.shape[1]
+    perm = np.arange(D, dtype=np.int32) if perm is None else np.asarray(perm, dtype=np.int32)
+    bnd = chunk_bounds(D, C)
+    Xall = A[:, perm].astype(np.float64)
+    Bp = B[perm]
+    split = np.zeros((C, N_LEVELS), np.int32)
+    thr = np.zeros((C, 2 ** N_LEVELS - 1), np.float32)
+    T = np.zeros((C, N_PROTO, M))
+    for c in range(C):
+        sd, th, P = _fit_subspace(Xall[:, bnd[c]:bnd[c + 1]])
+        split[c], thr[c] = sd, th.astype(np.float32)
+        Bc = Bp[bnd[c]:bnd[c + 1]]
+        for j in range(P.shape[1]):
+            T[c] += P[:, j:j + 1] * Bc[j:j + 1, :]
+    lo = T.min(axis=(0, 1))
+    hi = T.max(axis=(0, 1))
+    scale = np.where(hi > lo, (hi - lo) / 255.0, 1.0)
+    q = np.clip(np.floor((T - lo) / scale + 0.5), 0, 255).astype(np.uint8)
+    return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr,
+                lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
+                bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)))

@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Parameters are fitted by the ORACLE's fitter (oracle/fit.py), so no oracle input comes from
+the product.  Bar (BASELINE north_star): codes and int32 accumulators bit-exact; fp32 outputs
+within 1e-6 relative + 1e-6 absolute (checked), and — because both sides evaluate the same
+single fmaf (reading R8) — bit-exact as well (checked)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import fit as ofit
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL = ATOL = 1e-6
+ALGOS = ["simt", "tc"]
+
+
+def _plan(params, algo):
+    from paper_2207_05808_b200 import Plan
+    from paper_2207_05808_b200._lib import ItlummError, EUNSUPPORTED
+    p = Plan(params, device=0)
+    try:
+        p.set_algo(algo)
+    except ItlummError:
+        raise
+    return p
+
+
+def _dev(A, dtype):
+    t = torch.from_numpy(np.ascontiguousarray(A.view(np.int16) if dtype == "bf16" else A)).cuda()
+    return t.view(torch.bfloat16) if dtype == "bf16" else t
+
+
+def unpack(codes: np.ndarray, C: int) -> np.ndarray:
+    out = np.zeros((codes.shape[0], C), np.uint8)
+    for c in range(C):
+        b = codes[:, c // 2]
+        out[:, c] = (b >> 4) if c % 2 else (b & 15)
+    return out
+
+
+def assert_out(gpu, ref):
+    assert gpu.shape == ref.shape
+    assert np.allclose(gpu, ref, rtol=RTOL, atol=ATOL), np.abs(gpu - ref).max()
+    assert np.array_equal(gpu.view(np.uint32), ref.view(np.uint32)), int((gpu != ref).sum())
+
+
+def run_all(params, A, relu, dtype, algo):
+    """encode -> codes; lut_accumulate -> acc, out; amm (fused) -> out; all vs the oracle."""
+    from paper_2207_05808_b200._lib import ItlummError
+    ref = oracle.amm(params, A, relu=relu, dtype=dtype, want_codes=True, want_acc=True, nthreads=8)
+    plan = _plan(params, "simt")
+    Ad = _dev(A, dtype)
+    codes = plan.encode(Ad)
+    torch.cuda.synchronize()
+    assert np.array_equal(unpack(codes.cpu().numpy(), params["C"]), ref["codes"])
+    if params["C"] % 2:
+        assert np.all(codes.cpu().numpy()[:, -1] >> 4 == 0)     # R14 padding nibble
+    try:
+        plan.set_algo(algo)
+        acc = torch.empty((A.shape[0], params["M"]), dtype=torch.int32, device="cuda")
+        out, _ = plan.lut_accumulate(codes, acc=acc, relu=relu)
+        y = plan.amm(Ad, relu=relu)
+    except ItlummError as e:
+        if algo == "tc" and e.status == 3:
+            pytest.skip(f"tc path unsupported for this shape: {e}")
+        raise
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref["acc"])
+    assert_out(out.cpu().numpy(), ref["y"])
+    assert_out(y.cpu().numpy(), ref["y"])
+    return plan, ref
+
+
+CASES = [
+    # seed, N, D, M, C, dtype   (ragged N vs every tile height, odd C, M not a multiple of 16)
+    (1, 1000, 64, 24, 8, "f32"),
+    (2, 777, 97, 33, 10, "f32"),
+    (3, 1500, 96, 40, 12, "bf16"),
+    (4, 300, 50, 5, 50, "f32"),
+    (5, 2049, 784, 512, 32, "f32"),
+    (6, 513, 200, 1000, 17, "f32"),
+    (7, 129, 300, 129, 300, "f32"),       # C > 257: 16-bit SWAR lanes flushed
+    (8, 1, 31, 1, 1, "f32"),
+    (9, 4097, 256, 256, 64, "bf16"),
+]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("seed,N,D,M,C,dtype", CASES)
+def test_parity_small(seed, N, D, M, C, dtype, algo):
+    w = synth.small_case(seed, N=N, D=D, M=M, C=C, dtype=dtype, n_train=600)
+    params = ofit.fit(w["A_train"], w["B"], C, w["perm"], w["bias"], a_is_bf16=dtype == "bf16")
+    run_all(params, w["A"], w["relu"], dtype, algo)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_parity_cfg1_full(algo):
+    """BASELINE configs[0] at its full size (N = 1000)."""
+    w = synth.workload("cfg1")
+    params = ofit.fit(w["A_train"], w["B"], w["C"], w["perm"], w["bias"])
+    run_all(params, w["A"], w["relu"], "f32", algo)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_parity_cfg2_full_sampled(algo):
+    """BASELINE configs[1] at full size N = 60000 in the bench launch configuration: sampled rows
+    against the oracle, every row's fused output against encode -> lut_accumulate."""
+    from paper_2207_05808_b200._lib import ItlummError
+    w = synth.workload("cfg2")
+    params = ofit.fit(w["A_train"], w["B"], w["C"], w["perm"], w["bias"])
+    plan = _plan(params, "simt")
+    Ad = _dev(w["A"], "f32")
+    codes = plan.encode(Ad)
+    try:
+        plan.set_algo(algo)
+        y = plan.amm(Ad, relu=True)
+        y2, _ = plan.lut_accumulate(codes, relu=True)
+    except ItlummError as e:
+        if algo == "tc" and e.status == 3:
+            pytest.skip(str(e))
+        raise
+    torch.cuda.synchronize()
+    y, y2, codes = y.cpu().numpy(), y2.cpu().numpy(), codes.cpu().numpy()
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
+    rows = np.unique(np.concatenate([np.random.default_rng(0).choice(60000, 1500, replace=False),
+                                     [0, 1, 59998, 59999]]))
+    ref = oracle.amm(params, w["A"][rows], relu=True, want_codes=True, nthreads=8)
+    assert np.array_equal(unpack(codes[rows], 32), ref["codes"])
+    assert_out(y[rows], ref["y"])
+    assert np.all(y >= 0) and not np.any(np.signbit(y))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_edge_strides_alignment_and_specials(algo):
+    """lda > D, ldo > M, a misaligned output base (scalar-store path), +-inf thresholds, NaN and
+    +-inf inputs, N = 0."""
+    from paper_2207_05808_b200._lib import ItlummError
+    w = synth.small_case(11, N=600, D=80, M=48, C=10, n_train=500)
+    params = ofit.fit(w["A_train"], w["B"], 10, w["perm"], w["bias"])
+    params["thresholds"][0, :] = np.inf
+    params["thresholds"][1, :] = -np.inf
+    A = np.zeros((600, 91), np.float32)
+    A[:, :80] = w["A"]
+    A[3, :] = np.nan
+    A[4, :] = np.inf
+    A[5, :] = -np.inf
+    ref = oracle.amm(params, A, relu=True, want_codes=True)
+    plan = _plan(params, "simt")
+    try:
+        plan.set_algo(algo)
+        Ad = torch.from_numpy(A).cuda()
+        big = torch.full((600, 64), -7.0, device="cuda")
+        plan.amm(Ad[:, :], out=big[:, :48], relu=True)
+        raw = torch.full((600 * 48 + 1,), -7.0, device="cuda")
+        mis = raw[1:].view(600, 48)
+        plan.amm(Ad, out=mis, relu=True)
+        empty = plan.amm(Ad[:0], relu=True)
+    except ItlummError as e:
+        if algo == "tc" and e.status == 3:
+            pytest.skip(str(e))
+        raise
+    torch.cuda.synchronize()
+    assert_out(big[:, :48].cpu().numpy(), ref["y"])
+    assert np.all(big[:, 48:].cpu().numpy() == -7.0)
+    assert_out(mis.cpu().numpy(), ref["y"])
+    assert raw[0].item() == -7.0 and empty.shape == (0, 48)
+    assert plan.last_launch_count == 0   # N = 0 launches nothing
+
+
+def test_amm_host_end_to_end():
+    """itlumm_amm_host (host buffers, chunked H2D / kernel / D2H) equals the oracle."""
+    w = synth.small_case(12, N=70000, D=64, M=40, C=8, n_train=500)
+    params = ofit.fit(w["A_train"], w["B"], 8, w["perm"], w["bias"])
+    from paper_2207_05808_b200 import Plan
+    plan = Plan(params)
+    A = torch.from_numpy(w["A"]).pin_memory()
+    y = plan.amm_host(A, relu=True)
+    assert plan.last_launch_count >= 1
+    ref = oracle.amm(params, w["A"], relu=True, nthreads=8)
+    assert_out(y.numpy(), ref["y"])
+
+
+def test_error_paths_on_device():
+    from paper_2207_05808_b200 import Plan
+    from paper_2207_05808_b200._lib import ItlummError
+    w = synth.small_case(13, N=10, D=40, M=8, C=4, n_train=200)
+    params = ofit.fit(w["A_train"], w["B"], 4, w["perm"], w["bias"])
+    plan = Plan(params)
+    A = torch.from_numpy(w["A"]).cuda()
+    with pytest.raises(ItlummError):
+        plan.amm(A[:, :30].contiguous())             # lda < D
+    with pytest.raises(TypeError):
+        plan.amm(A.double())
+    with pytest.raises(ItlummError):
+        plan.amm(A, out=torch.empty((10, 4), device="cuda"))   # ldo < M
