@@ -42,7 +42,7 @@ static itlumm_status fail(itlumm_status st, const char* fmt, ...) {
 
 // ------------------------------------------------------------------------------ plan
 struct SimtCfg {
-  int MS = 0, R = 0, S = 0, G = 0;
+  int MS = 0, R = 0, S = 0, G = 0, RPT = 1;
   size_t smem_fused = 0, smem_codes = 0;
   int grid_fused = 0, grid_codes = 0;
 };
@@ -99,13 +99,20 @@ static itlumm_status configure_simt(itlumm_plan_s* P) {
   const int C4 = (C + 3) & ~3;
   for (int MS = mp2; MS >= 16; MS >>= 1) {
     const int LPR = MS / 16;
-    int R = kConsumers / LPR;
+    const int RPP = kConsumers / LPR;
+    // rows per tile: grow by whole consumer passes until a tile holds >= one producer chunk
+    // of (row, codebook) pairs, keeping the offset ring <= 48 KB
+    int RPT = 1;
+    while (RPT < 8 && (int64_t)RPP * RPT * C4 < kChunkPairs) RPT <<= 1;
+    int R = RPP * RPT;
     int S = 4;
-    // offset ring <= 48 KB
-    while (R > 1 && (size_t)S * R * C4 * 4 > 48 * 1024) R >>= 1;
+    while (R > 1 && (size_t)S * R * C4 * 4 > 48 * 1024) {
+      if (RPT > 1) RPT >>= 1;
+      R >>= 1;
+    }
     if (lut_smem_bytes(C, MS, R, S, true) <= budget) {
       SimtCfg& s = P->simt;
-      s.MS = MS; s.R = R; s.S = S;
+      s.MS = MS; s.R = R; s.S = S; s.RPT = RPT;
       s.G = (P->Mp + MS - 1) / MS;
       s.smem_fused = lut_smem_bytes(C, MS, R, S, true);
       s.smem_codes = lut_smem_bytes(C, MS, R, S, false);
@@ -353,7 +360,7 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
   const bool out_al = !out || (((uintptr_t)out % 16) == 0 && ldo % 4 == 0);
   const bool acc_al = !acc || (((uintptr_t)acc % 16) == 0 && ldacc % 4 == 0);
   g.vec_out = out_al && acc_al;
-  g.R = c.R; g.S = c.S; g.G = c.G; g.one = 1u;
+  g.R = c.R; g.RPT = c.RPT; g.S = c.S; g.G = c.G; g.one = 1u;
   const int64_t ntiles = (N + c.R - 1) / c.R;
   int grid = fused ? c.grid_fused : c.grid_codes;
   const int64_t maxgrid = (int64_t)c.G * ntiles;

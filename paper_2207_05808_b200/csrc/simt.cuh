@@ -47,6 +47,8 @@ constexpr int kProducers = 128;   // 4 producer warps
 constexpr int kConsumers = 256;   // 8 consumer warps
 constexpr int kLutThreads = kProducers + kConsumers;
 constexpr int kMaxStages = 7;     // named barrier ids 1..2*S
+constexpr int kPairsPerThread = 8;                        // (row, codebook) pairs per producer chunk
+constexpr int kChunkPairs = kProducers * kPairsPerThread; // pairs per producer chunk
 
 struct LutArgs {
   const void* A;          // FUSED: activations
@@ -60,7 +62,8 @@ struct LutArgs {
   int64_t ldo;
   int relu;
   int vec_out;            // out/acc rows 16-byte aligned -> 128-bit stores
-  int R;                  // rows per tile
+  int R;                  // rows per tile (= rows per consumer pass * RPT)
+  int RPT;                // rows per consumer thread per tile
   int S;                  // ring stages
   int G;                  // M slices (grid = G * groups)
   uint32_t one;           // runtime constant 1 (see add_fma_pipe)
@@ -71,7 +74,7 @@ __host__ __device__ inline size_t lut_smem_bytes(int C, int MS, int R, int S, bo
   const int C4 = (C + 3) & ~3;
   size_t b = (size_t)(C * 16 + 1) * MS;          // LUT slice + one zero row (padding target)
   b = (b + 15) & ~(size_t)15;
-  if (fused) b += (size_t)15 * C * 4 + (size_t)C * 16;  // thresholds [15][C] + cols [C][4]
+  if (fused) b += (size_t)C * 16 + (size_t)15 * C * 4;  // cols [C][4] (16B aligned) + thr [15][C]
   b = (b + 15) & ~(size_t)15;
   b += (size_t)S * R * C4 * 4;                    // offset ring
   return b;
@@ -93,9 +96,9 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
 
   uint8_t* lut_s = smem;
   size_t off = ((size_t)(C * 16 + 1) * MS + 15) & ~(size_t)15;
-  float* thr_s = reinterpret_cast<float*>(smem + off);
-  int32_t* cols_s = reinterpret_cast<int32_t*>(smem + off + (size_t)15 * C * 4);
-  if (FUSED) off += (size_t)15 * C * 4 + (size_t)C * 16;
+  int32_t* cols_s = reinterpret_cast<int32_t*>(smem + off);              // 16-byte aligned
+  float* thr_s = reinterpret_cast<float*>(smem + off + (size_t)C * 16);
+  if (FUSED) off += (size_t)C * 16 + (size_t)15 * C * 4;
   off = (off + 15) & ~(size_t)15;
   uint32_t* ring = reinterpret_cast<uint32_t*>(smem + off);
   const uint32_t zero_row = (uint32_t)(C * 16 * MS);
@@ -123,53 +126,72 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
   const int tid = threadIdx.x;
   if (tid < kProducers) {
     // ================================================================ producer warps
-    int k = 0;
-    for (int64_t tile = group; tile < ntiles; tile += ngroups, ++k) {
-      const int s = k % S;
-      if (k >= S) named_bar_sync(1 + S + s, kLutThreads);     // consumers released stage s
-      uint32_t* st = ring + (size_t)s * R * C4;
-      const int64_t row0 = tile * R;
-      if (FUSED) {
-        const T* A = reinterpret_cast<const T*>(g.A);
-        const int npair = R * C4;
-        constexpr int U = 4;
-        for (int base = tid; base < npair; base += kProducers * U) {
-          float v[U][4];
-          int pr[U], pc[U];
-          bool ok[U];
+    if (FUSED) {
+      // The tile sequence is cut into chunks of kChunkPairs (row, codebook) pairs.  The gather
+      // of chunk j+1 is issued before the tree walks of chunk j, so the 4 split-column loads of
+      // ~2K pairs per CTA are always in flight (latency hiding without occupancy).
+      const T* A = reinterpret_cast<const T*>(g.A);
+      const int npair = R * C4;
+      const int nch = (npair + kChunkPairs - 1) / kChunkPairs;
+      float vc[kPairsPerThread][4], vn[kPairsPerThread][4];
+      auto load_chunk = [&](int64_t tile, int ch, float (&v)[kPairsPerThread][4]) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int q = base + u * kProducers;
-            pr[u] = q / C4;
-            pc[u] = q - pr[u] * C4;
-            const int64_t row = row0 + pr[u];
-            ok[u] = (q < npair) && (pc[u] < C) && (row < g.N);
-            if (ok[u]) {
-              const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * pc[u]);
-              const T* a = A + row * g.lda;
-              v[u][0] = InTraits<T>::load(a + col.x);
-              v[u][1] = InTraits<T>::load(a + col.y);
-              v[u][2] = InTraits<T>::load(a + col.z);
-              v[u][3] = InTraits<T>::load(a + col.w);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int q = base + u * kProducers;
-            if (q < npair) {
-              uint32_t o = zero_row;
-              if (ok[u]) {
-                const int code = tree_walk(v[u], thr_s, C, pc[u]);
-                o = (uint32_t)((pc[u] * 16 + code) * MS);
-              }
-              st[q] = o;
-            }
+        for (int u = 0; u < kPairsPerThread; ++u) {
+          const int q = ch * kChunkPairs + u * kProducers + tid;
+          const int r = q / C4, c = q - r * C4;
+          const int64_t row = tile * R + r;
+          if (q < npair && c < C && row < g.N) {
+            const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+            const T* a = A + row * g.lda;
+            v[u][0] = InTraits<T>::load(a + col.x);
+            v[u][1] = InTraits<T>::load(a + col.y);
+            v[u][2] = InTraits<T>::load(a + col.z);
+            v[u][3] = InTraits<T>::load(a + col.w);
           }
         }
-      } else {
-        const int nbp = C4 >> 1;             // byte pairs per row (codebooks 2b, 2b+1)
-        const int nb = (C + 1) >> 1;         // real code bytes per row
-        const int n = R * nbp;
+      };
+      int64_t tile = group;
+      int ch = 0, k = 0;
+      if (tile < ntiles) load_chunk(tile, 0, vc);
+      while (tile < ntiles) {
+        // next chunk position
+        int64_t ntile = tile;
+        int nch_i = ch + 1;
+        if (nch_i == nch) { nch_i = 0; ntile += ngroups; }
+        if (ntile < ntiles) load_chunk(ntile, nch_i, vn);
+        const int s = k % S;
+        if (ch == 0 && k >= S) named_bar_sync(1 + S + s, kLutThreads);   // stage s released
+        uint32_t* st = ring + (size_t)s * R * C4;
+#pragma unroll
+        for (int u = 0; u < kPairsPerThread; ++u) {
+          const int q = ch * kChunkPairs + u * kProducers + tid;
+          if (q < npair) {
+            const int r = q / C4, c = q - r * C4;
+            uint32_t o = zero_row;
+            if (c < C && tile * R + r < g.N)
+              o = (uint32_t)((c * 16 + tree_walk(vc[u], thr_s, C, c)) * MS);
+            st[q] = o;
+          }
+        }
+        if (ch == nch - 1) { named_bar_arrive(1 + s, kLutThreads); ++k; }   // stage s full
+#pragma unroll
+        for (int u = 0; u < kPairsPerThread; ++u)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) vc[u][t] = vn[u][t];
+        tile = ntile;
+        ch = nch_i;
+      }
+      for (int j = (k > S ? k - S : 0); j < k; ++j) named_bar_sync(1 + S + (j % S), kLutThreads);
+    } else {
+      int k = 0;
+      const int nbp = C4 >> 1;             // byte pairs per row (codebooks 2b, 2b+1)
+      const int nb = (C + 1) >> 1;         // real code bytes per row
+      const int n = R * nbp;
+      for (int64_t tile = group; tile < ntiles; tile += ngroups, ++k) {
+        const int s = k % S;
+        if (k >= S) named_bar_sync(1 + S + s, kLutThreads);     // consumers released stage s
+        uint32_t* st = ring + (size_t)s * R * C4;
+        const int64_t row0 = tile * R;
         for (int q = tid; q < n; q += kProducers) {
           const int r = q / nbp, b = q - r * nbp;
           const int64_t row = row0 + r;
@@ -182,18 +204,16 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
           }
           *reinterpret_cast<uint2*>(st + r * C4 + 2 * b) = make_uint2(o0, o1);
         }
+        named_bar_arrive(1 + s, kLutThreads);                   // stage s full
       }
-      named_bar_arrive(1 + s, kLutThreads);                   // stage s full
+      for (int j = (k > S ? k - S : 0); j < k; ++j) named_bar_sync(1 + S + (j % S), kLutThreads);
     }
-    // drain the consumers' last releases so no barrier is left pending at exit
-    for (int j = (k > S ? k - S : 0); j < k; ++j) named_bar_sync(1 + S + (j % S), kLutThreads);
   } else {
     // ================================================================ consumer warps
     const int ctid = tid - kProducers;
-    const int rl = ctid / LPR;          // row within the tile
-    const int lane = ctid - rl * LPR;   // 16-column group within the slice
+    const int rl0 = ctid / LPR;         // first row within the tile
+    const int lane = ctid - rl0 * LPR;  // 16-column group within the slice
     const int mbase = m0 + lane * 16;
-    const bool active = rl < R;
     float sc[16], ot[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -202,14 +222,17 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
       ot[j] = (m < p.Mp) ? __ldg(p.offtot + m) : 0.f;
     }
     const uint32_t one = g.one;
+    const bool full = g.vec_out && (mbase + 16 <= p.M);
     int k = 0;
     for (int64_t tile = group; tile < ntiles; tile += ngroups, ++k) {
       const int s = k % S;
       named_bar_sync(1 + s, kLutThreads);
-      uint32_t acc[16];
+      for (int rr = 0; rr < g.RPT; ++rr) {
+        const int rl = rl0 + rr * RPP;
+        if (rl >= R) break;
+        uint32_t acc[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0;
-      if (active) {
+        for (int j = 0; j < 16; ++j) acc[j] = 0;
         const uint32_t* offs = ring + ((size_t)s * R + rl) * C4;
         const uint8_t* lbase = lut_s + lane * 16;
         for (int cb = 0; cb < C4; cb += 256) {      // 16-bit lanes are exact for <= 257 adds
@@ -238,44 +261,42 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
             acc[4 * i + 3] += od[i] >> 16;
           }
         }
+        const int64_t row = tile * R + rl;
+        if (row < g.N) {
+          if (g.out) {
+            float y[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              y[j] = fmaf(sc[j], __uint2float_rn(acc[j]), ot[j]);   // a4, one rounding (R8)
+              if (g.relu) y[j] = relu_pos0(y[j]);
+            }
+            float* o = g.out + row * g.ldo + mbase;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) st_cs_f4(o + j, y[j], y[j + 1], y[j + 2], y[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (mbase + j < p.M) o[j] = y[j];
+            }
+          }
+          if (g.acc) {
+            int32_t* a = g.acc + row * g.ldacc + mbase;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4)
+                __stcs(reinterpret_cast<int4*>(a + j), make_int4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (mbase + j < p.M) a[j] = (int32_t)acc[j];
+            }
+          }
+        }
       }
       named_bar_arrive(1 + S + s, kLutThreads);               // stage s free
-      const int64_t row = tile * R + rl;
-      if (active && row < g.N) {
-        const bool full = g.vec_out && (mbase + 16 <= p.M);
-        if (g.out) {
-          float y[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            y[j] = fmaf(sc[j], __uint2float_rn(acc[j]), ot[j]);   // a4, one rounding (R8)
-            if (g.relu) y[j] = relu_pos0(y[j]);
-          }
-          float* o = g.out + row * g.ldo + mbase;
-          if (full) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) st_cs_f4(o + j, y[j], y[j + 1], y[j + 2], y[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (mbase + j < p.M) o[j] = y[j];
-          }
-        }
-        if (g.acc) {
-          int32_t* a = g.acc + row * g.ldacc + mbase;
-          if (full) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              __stcs(reinterpret_cast<int4*>(a + j), make_int4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (mbase + j < p.M) a[j] = (int32_t)acc[j];
-          }
-        }
-      }
     }
   }
-  (void)RPP;
 }
 
 }  // namespace itlumm

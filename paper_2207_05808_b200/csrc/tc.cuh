@@ -1,16 +1,45 @@
-// tc.cuh — tcgen05 one-hot x LUT tensor-core path.  Placeholder until the
-// kernel lands: the plan reports the path as unsupported, AUTO selects SIMT.
+// tc.cuh — tcgen05 one-hot x LUT tensor-core kernel.
+//
+// The lookup-accumulate a3 is the product G.Q of the one-hot encoding G (N x 16C, "the
+// concatenation of C one-hot 16-dimensional vectors") with the uint8 LUT Q (16C x M):
+// acc = G.Q exactly, then the a4 epilogue.  Per persistent CTA:
+//   producer warps  : FUSED: gather the 4C split columns of each row and walk the trees (a1+a2);
+//                     else: read nibble-packed codes.  Either way they write the one-hot tile
+//                     (128 rows x 128 B = 8 codebooks per K-block) straight into shared memory
+//                     in the UMMA canonical K-major SWIZZLE_128B layout (one 16-byte chunk per
+//                     (row, codebook)), ring of SA K-block stages.
+//   MMA warp        : one elected thread issues tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32,
+//                     M=128, N=NS, K=32 per instruction = 2 codebooks) into a TMEM accumulator
+//                     (double buffered), B = the CTA's LUT slice, resident in shared memory.
+//   epilogue warps  : tcgen05.ld the s32 accumulators, y = fmaf(scale, (float)acc, offtot) (+ReLU),
+//                     store fp32 rows.
+// Integer products/sums of u8 one-hot x u8 LUT are exact, so results equal the SIMT path bit for bit.
 #pragma once
+#include <cstring>
 #include <vector>
-#include "common.cuh"
+
 #include "../../include/itlumm.h"
+#include "common.cuh"
 
 namespace itlumm {
 
+constexpr int kTcProducerWarps = 4;
+constexpr int kTcProducers = 32 * kTcProducerWarps;           // one producer thread per tile row
+constexpr int kTcMmaWarp = kTcProducerWarps;                   // warp 4
+constexpr int kTcEpiWarp0 = kTcProducerWarps + 1;              // warps 5..8
+constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + 4);    // 288
+constexpr int kTcRows = 128;                                   // UMMA M
+constexpr int kKBlock = 128;                                   // bytes of K per block = 8 codebooks
+constexpr int kTcStages = 4;                                   // A ring depth (K-blocks)
+constexpr size_t kTcBBudget = 144 * 1024;                      // resident LUT slice budget
+
 struct TcPlan {
   bool ok = false;
-  const char* why = "tcgen05 path not built";
-  const uint8_t* qt = nullptr;
+  const char* why = "not configured";
+  const uint8_t* qt = nullptr;   // device: [G][KB][NS][128] swizzled K-major LUT slices
+  int C = 0, M = 0, KB = 0, NS = 0, G = 0, tmem_cols = 0;
+  size_t smem = 0;
+  int grid = 0;
 };
 
 struct TcArgs {
@@ -18,12 +47,388 @@ struct TcArgs {
   int32_t* acc; int64_t ldacc; float* out; int64_t ldo; int relu;
 };
 
-inline const char* tc_last_msg() { return "tcgen05 path not built"; }
-inline void tc_layout_host(int, int, const uint8_t*, TcPlan*, std::vector<uint8_t>& qt) { qt.clear(); }
-inline itlumm_status tc_configure(TcPlan&, int) { return ITLUMM_OK; }
-inline bool tc_preferred(const TcPlan& t, bool) { return false && t.ok; }
-inline itlumm_status tc_launch(const TcPlan&, const DevPlan&, bool, bool, const TcArgs&, cudaStream_t) {
-  return ITLUMM_EUNSUPPORTED;
+struct TcKArgs {
+  const void* A; int64_t lda;
+  const uint8_t* codes; int64_t ldc;
+  int64_t N;
+  int32_t* acc; int64_t ldacc;
+  float* out; int64_t ldo;
+  int relu;
+  const uint8_t* qt;
+  int KB, NS, G, tmem_cols;
+};
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SMEM matrix descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), LBO unused (1),
+// version 1 (sm_100), base offset 0 (atoms are 1024-byte aligned).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor, kind::i8: D s32, A u8, B u8, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Byte offset of the 16-byte chunk j (0..7) of row r in a K-major SWIZZLE_128B tile.
+__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t j) {
+  return (r >> 3) * 1024u + (r & 7u) * 128u + ((j ^ (r & 7u)) << 4);
+}
+
+// Shared-memory carve-up (offsets from a 1024-aligned base).
+struct TcSmem {
+  size_t b, a, thr, cols, sc, ot, bar, tmem, total;
+};
+__host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS) {
+  TcSmem s{};
+  size_t o = 0;
+  s.b = o;    o += (size_t)KB * NS * kKBlock;
+  s.a = o;    o += (size_t)kTcStages * kTcRows * kKBlock;
+  s.thr = o;  o += (size_t)C * 16 * 4;          // thresholds [C][16] (15 used)
+  s.cols = o; o += (size_t)C * 16;              // cols [C][4]
+  s.sc = o;   o += (size_t)NS * 4;
+  s.ot = o;   o += (size_t)NS * 4;
+  o = (o + 7) & ~(size_t)7;
+  s.bar = o;  o += (size_t)(2 * kTcStages + 4) * 8;
+  s.tmem = o; o += 16;
+  s.total = o + 1024;                           // slack for 1024-byte alignment of the base
+  return s;
+}
+
+template <bool FUSED, typename T>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
+  const TcSmem L = tc_smem_layout(C, KB, NS);
+  uint8_t* b_s = smem + L.b;
+  uint8_t* a_s = smem + L.a;
+  float* thr_s = reinterpret_cast<float*>(smem + L.thr);
+  int32_t* cols_s = reinterpret_cast<int32_t*>(smem + L.cols);
+  float* sc_s = reinterpret_cast<float*>(smem + L.sc);
+  float* ot_s = reinterpret_cast<float*>(smem + L.ot);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty_bar = full_bar + kTcStages;
+  uint64_t* accf_bar = empty_bar + kTcStages;
+  uint64_t* acce_bar = accf_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
+
+  const int slice = blockIdx.x % G;
+  const int group = blockIdx.x / G;
+  const int ngroups = gridDim.x / G;
+  const int m0 = slice * NS;
+  const int64_t ntiles = (g.N + kTcRows - 1) / kTcRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- prologue: resident LUT slice (already swizzled in HBM), thresholds, columns, scales
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(g.qt + (size_t)slice * KB * NS * kKBlock);
+    uint4* dst = reinterpret_cast<uint4*>(b_s);
+    const int nv = KB * NS * kKBlock / 16;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (FUSED) {
+      for (int i = threadIdx.x; i < C * 16; i += blockDim.x) {
+        const int c = i >> 4, h = i & 15;
+        thr_s[i] = h < 15 ? __ldg(p.thr_t + h * C + c) : 0.f;
+      }
+      for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) cols_s[i] = __ldg(p.cols + i);
+    }
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) {
+      const int m = m0 + i;
+      sc_s[i] = m < p.Mp ? __ldg(p.scale + m) : 0.f;
+      ot_s[i] = m < p.Mp ? __ldg(p.offtot + m) : 0.f;
+    }
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers); mbar_init(empty_bar + s, 1); }
+      for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, 128); }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kTcMmaWarp) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(g.tmem_cols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_proxy_async_smem();   // B slice written by generic stores, read by the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < kTcProducerWarps) {
+    // ============================================================== producers: one row each
+    const int r = threadIdx.x;                       // row within the tile, 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      const int64_t row = tile * kTcRows + r;
+      const bool valid = row < g.N;
+      const T* a = FUSED ? reinterpret_cast<const T*>(g.A) + (valid ? row : 0) * g.lda : nullptr;
+      for (int kb = 0; kb < KB; ++kb) {
+        // codes of codebooks 8kb .. 8kb+7 of this row
+        uint32_t code[8];
+        if (FUSED) {
+          float v[8][4];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = kb * 8 + j;
+            if (valid && c < C) {
+              const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+              v[j][0] = InTraits<T>::load(a + col.x);
+              v[j][1] = InTraits<T>::load(a + col.y);
+              v[j][2] = InTraits<T>::load(a + col.z);
+              v[j][3] = InTraits<T>::load(a + col.w);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = kb * 8 + j;
+            code[j] = 16;                             // 16 = no one-hot bit (padding)
+            if (valid && c < C) {
+              const float* th = thr_s + c * 16;
+              int node = 0;
+#pragma unroll
+              for (int t = 0; t < kLevels; ++t) node = 2 * node + (v[j][t] > th[(1 << t) - 1 + node] ? 1 : 0);
+              code[j] = (uint32_t)node;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = kb * 8 + j;
+            code[j] = 16;
+            if (valid && c < C) {
+              const uint32_t byte = g.codes[row * g.ldc + (c >> 1)];
+              code[j] = (c & 1) ? (byte >> 4) : (byte & 15u);
+            }
+          }
+        }
+        mbar_wait(empty_bar + stage, phase ^ 1);      // MMA finished reading this stage
+        uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t k = code[j];
+          const uint32_t bit = (k < 16) ? (1u << ((k & 3u) * 8u)) : 0u;
+          const uint32_t w = k >> 2;
+          const uint4 oh = make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
+          *reinterpret_cast<uint4*>(st + sw128_off(r, j)) = oh;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(full_bar + stage);
+        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == kTcMmaWarp) {
+    // ============================================================== MMA issuer
+    const uint32_t idesc = idesc_i8(NS);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      mbar_wait(acce_bar + acc, acc_phase ^ 1);      // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)(acc * NS);
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(full_bar + stage, phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kTcRows * kKBlock);
+          const uint32_t b_addr = smem_u32(b_s + (size_t)kb * NS * kKBlock);
+#pragma unroll
+          for (int ks = 0; ks < kKBlock / 32; ++ks)
+            umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
+                    (kb | ks) != 0);
+          umma_commit(empty_bar + stage);             // frees the A stage when these MMAs finish
+          if (kb == KB - 1) umma_commit(accf_bar + acc);
+        }
+        __syncwarp();
+        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ============================================================== epilogue: one row per thread
+    const int q = warp & 3;                           // TMEM lane quadrant of this warp
+    const int r = q * 32 + lane;                      // row within the tile
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      mbar_wait(accf_bar + acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = tile * kTcRows + r;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
+      for (int j0 = 0; j0 < NS; j0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tbase + j0, v);
+        tmem_wait_ld();
+        if (row < g.N) {
+          const int mb = m0 + j0;
+          if (g.out) {
+            float y[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              y[j] = fmaf(sc_s[j0 + j], __uint2float_rn(v[j]), ot_s[j0 + j]);   // a4 (R8)
+              if (g.relu) y[j] = relu_pos0(y[j]);
+            }
+            float* o = g.out + row * g.ldo + mb;
+            const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (mb + 16 <= p.M);
+            if (vec) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) st_cs_f4(o + j, y[j], y[j + 1], y[j + 2], y[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (mb + j < p.M) o[j] = y[j];
+            }
+          }
+          if (g.acc) {
+            int32_t* a = g.acc + row * g.ldacc + mb;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (mb + j < p.M) a[j] = (int32_t)v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acce_bar + acc);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kTcMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(g.tmem_cols) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+static thread_local const char* g_tc_msg = "";
+inline const char* tc_last_msg() { return g_tc_msg; }
+
+// Choose the N slice and build the swizzled K-major LUT image: qt[s][kb][n][128 B] with
+// byte (n, k) at sw128_off(n, k/16) + k%16 of block (s, kb); k = 16*(c - 8kb) + code.
+inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vector<uint8_t>& qt) {
+  qt.clear();
+  t->C = C; t->M = M;
+  t->KB = (16 * C + kKBlock - 1) / kKBlock;
+  int ns_max = (int)(kTcBBudget / ((size_t)t->KB * kKBlock)) / 16 * 16;
+  if (ns_max > 256) ns_max = 256;
+  if (ns_max < 16) { t->ok = false; t->why = "C too large for a resident LUT slice (C > ~1150)"; return; }
+  const int G = (M + ns_max - 1) / ns_max;
+  int NS = (M + G - 1) / G;
+  NS = (NS + 15) / 16 * 16;
+  if (NS < 16) NS = 16;
+  t->G = G; t->NS = NS;
+  int cols = 32;
+  while (cols < 2 * NS) cols <<= 1;
+  t->tmem_cols = cols;
+  const size_t blk = (size_t)NS * kKBlock;
+  qt.assign((size_t)G * t->KB * blk, 0);
+  for (int s = 0; s < G; ++s)
+    for (int n = 0; n < NS; ++n) {
+      const int m = s * NS + n;
+      if (m >= M) continue;
+      for (int c = 0; c < C; ++c) {
+        const int kb = c / 8, jc = c % 8;
+        uint8_t* base = qt.data() + ((size_t)s * t->KB + kb) * blk + sw128_off(n, jc);
+        for (int code = 0; code < 16; ++code) base[code] = lut[((size_t)c * 16 + code) * M + m];
+      }
+    }
+  t->ok = true;
+  t->why = "";
+}
+
+template <bool FUSED, typename T>
+inline itlumm_status tc_set_attr(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc<FUSED, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
+  return ITLUMM_OK;
+}
+
+inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
+  if (!t.ok) return ITLUMM_OK;
+  t.smem = tc_smem_layout(t.C, t.KB, t.NS).total;
+  if (t.smem > 227 * 1024) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
+  itlumm_status st;
+  if ((st = tc_set_attr<true, float>(t.smem)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, uint16_t>(t.smem)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<false, float>(t.smem)) != ITLUMM_OK) return st;
+  t.grid = t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
+  return ITLUMM_OK;
+}
+
+// AUTO policy: the tensor-core path when its tiling applies.
+inline bool tc_preferred(const TcPlan& t, bool simt_ok) { return t.ok || !simt_ok; }
+
+inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, bool bf16, const TcArgs& a,
+                               cudaStream_t s) {
+  TcKArgs k{};
+  k.A = a.A; k.lda = a.lda; k.codes = a.codes; k.ldc = a.ldc; k.N = a.N;
+  k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
+  k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
+  const int64_t ntiles = (a.N + kTcRows - 1) / kTcRows;
+  int64_t grid = t.grid;
+  if (grid > (int64_t)t.G * ntiles) grid = (int64_t)t.G * ntiles;
+  if (fused) {
+    if (bf16) k_tc<true, uint16_t><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
+    else k_tc<true, float><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
+  } else {
+    k_tc<false, float><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
+  return ITLUMM_OK;
 }
 
 }  // namespace itlumm

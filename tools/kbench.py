@@ -1,0 +1,64 @@
+#!/usr/bin/env python
+"""Per-kernel timing probe (CUDA events): encode, lut_accumulate, fused amm for one workload and
+algo.  Diagnostic only (bench.py is the contract); prints one JSON dict per line."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2207_05808_b200 import Plan, fit_layer  # noqa: E402
+
+
+def timeit(fn, iters, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--algos", default="simt,tc")
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--rows", type=int, default=None)
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.workload]
+    n = cfg["N"] if args.rows is None else args.rows
+    bf16 = cfg["dtype"] == "bf16"
+    w = synth.workload(args.workload, n_rows=n)
+    params = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
+    plan = Plan(params)
+    A = torch.from_numpy(w["A"].view(np.int16) if bf16 else w["A"]).cuda()
+    if bf16:
+        A = A.view(torch.bfloat16)
+    out = torch.empty((n, cfg["M"]), device="cuda")
+    codes = plan.encode(A)
+    s_a = 2 if bf16 else 4
+    res = {"workload": args.workload, "rows": n}
+    res["encode_ms"] = timeit(lambda: plan.encode(A, codes=codes), args.iters)
+    for algo in args.algos.split(","):
+        try:
+            plan.set_algo(algo)
+            res[f"{algo}_accumulate_ms"] = timeit(lambda: plan.lut_accumulate(codes, out=out, relu=cfg["relu"]), args.iters)
+            res[f"{algo}_fused_ms"] = timeit(lambda: plan.amm(A, out=out, relu=cfg["relu"]), args.iters)
+            ab = n * (4 * cfg["C"] * s_a + 4 * cfg["M"]) + 16 * cfg["C"] * cfg["M"]
+            res[f"{algo}_fused_GBps_alg"] = ab / (res[f"{algo}_fused_ms"] * 1e-3) / 1e9
+        except Exception as e:  # report, keep going
+            res[f"{algo}_error"] = str(e)
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
