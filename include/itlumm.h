@@ -50,13 +50,20 @@ typedef enum {
 typedef enum { ITLUMM_F32 = 0, ITLUMM_BF16 = 1 } itlumm_dtype;            /* element type of A */
 typedef enum { ITLUMM_EPI_NONE = 0, ITLUMM_EPI_RELU = 1 } itlumm_epilogue;  /* sigma    */
 
-/* Kernel family used by itlumm_amm / itlumm_lut_accumulate.
- *   AUTO  : library choice (documented in DESIGN.md "kernel selection")
- *   SIMT  : CUDA-core shared-memory LUT kernels (any shape within the limits below)
- *   TC    : tcgen05 one-hot x LUT int8 tensor-core kernel (G.T with G the one-hot encoding,
- *           P:89; exact integer products) — EUNSUPPORTED where its tiling does not apply.
- * Both families produce bit-identical results. */
-typedef enum { ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2 } itlumm_algo;
+/* Kernel schedule used by itlumm_amm / itlumm_amm_host / itlumm_lut_accumulate.
+ *   AUTO    : library choice: TC_PIPE when the tensor-core
+ *             tiling splits M over several CTAs, else TC; SIMT where TC does not apply.
+ *   SIMT    : CUDA-core shared-memory LUT kernels; itlumm_amm = one fused kernel.
+ *   TC      : tcgen05 one-hot x LUT int8 tensor-core kernel (G.T with G the one-hot encoding,
+ *             P:89; exact integer products); itlumm_amm = one fused kernel (encode inside).
+ *   TC_PIPE : itlumm_amm = the encode kernel writing codes to a plan-owned, L2-resident scratch
+ *             buffer, then the TC accumulate kernel (2 launches; concurrent calls on one plan
+ *             are serialised on the device through an event).  itlumm_lut_accumulate = TC.
+ * TC and TC_PIPE return EUNSUPPORTED where the tensor-core tiling does not apply.  Every
+ * schedule produces bit-identical results. */
+typedef enum {
+  ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2, ITLUMM_ALGO_TC_PIPE = 3
+} itlumm_algo;
 
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */
 
@@ -110,8 +117,10 @@ itlumm_status itlumm_lut_accumulate(itlumm_plan plan, const uint8_t* codes, int6
                                     int64_t N, int32_t* acc, int64_t ldacc, float* out,
                                     int64_t ldo, itlumm_epilogue epi, void* stream);
 
-/* Fused a1..a4: one kernel, codes never reach HBM.  A as in itlumm_encode, out device fp32
- * [N][ldo], ldo >= M.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+/* a1..a4 in one call.  With SIMT/TC one fused kernel (codes never leave the SM); with
+ * TC_PIPE (AUTO's choice when M is split across CTAs) encode + accumulate kernels exchanging
+ * the codes (ceil(C/2) bytes per row) through an L2-resident scratch buffer.  A as in
+ * itlumm_encode, out device fp32 [N][ldo], ldo >= M.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
 itlumm_status itlumm_amm(itlumm_plan plan, const void* A, itlumm_dtype dtype, int64_t lda,
                          int64_t N, float* out, int64_t ldo, itlumm_epilogue epi, void* stream);
 

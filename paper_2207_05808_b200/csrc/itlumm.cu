@@ -56,6 +56,12 @@ struct itlumm_plan_s {
   DevPlan dp{};
   SimtCfg simt{};
   TcPlan tc{};
+  // TC_PIPE code scratch (allocated at plan creation; reuse ordered by scratch_ev)
+  std::mutex scratch_mu;
+  uint8_t* scratch = nullptr;
+  int64_t scratch_rows = 0, scratch_ldc = 0;
+  cudaEvent_t scratch_ev = nullptr;
+  bool scratch_used = false;
   // host API staging
   std::mutex host_mu;
   cudaStream_t hs[2] = {nullptr, nullptr};
@@ -215,6 +221,8 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   cudaGetDevice(&prev);
   auto cleanup = [&](itlumm_status st) {
     if (P->dmem) cudaFree(P->dmem);
+    if (P->scratch) cudaFree(P->scratch);
+    if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
     delete P;
     cudaSetDevice(prev);
     return st;
@@ -245,6 +253,14 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
+  if (P->tc.ok) {
+    P->scratch_ldc = (((C + 1) / 2) + 15) & ~15;
+    P->scratch_rows = 262144;
+    e = cudaMalloc(&P->scratch, (size_t)P->scratch_rows * P->scratch_ldc);
+    if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "scratch cudaMalloc: %s", cudaGetErrorString(e)));
+    e = cudaEventCreateWithFlags(&P->scratch_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
+  }
   cudaSetDevice(prev);
   *out = P;
   return ITLUMM_OK;
@@ -258,6 +274,8 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
   cudaSetDevice(P->device);
   cudaDeviceSynchronize();
   if (P->dmem) cudaFree(P->dmem);
+  if (P->scratch) cudaFree(P->scratch);
+  if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
   if (P->stage) cudaFree(P->stage);
   for (auto& s : P->hs)
     if (s) cudaStreamDestroy(s);
@@ -270,7 +288,7 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
 extern "C" itlumm_status itlumm_plan_set_algo(itlumm_plan P, itlumm_algo algo) {
   g_err.clear();
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
-  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC)
+  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC && algo != ITLUMM_ALGO_TC_PIPE)
     return fail(ITLUMM_EINVAL, "bad algo %d", (int)algo);
   P->algo = algo;
   return ITLUMM_OK;
@@ -334,8 +352,17 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
 
 static bool use_tc(itlumm_plan P) {
   if (P->algo == ITLUMM_ALGO_SIMT) return false;
-  if (P->algo == ITLUMM_ALGO_TC) return true;
+  if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE) return true;
   return tc_preferred(P->tc, P->simt.MS != 0);
+}
+
+// The fused call runs as encode -> TC accumulate when asked to (TC_PIPE), or under AUTO when
+// the tensor-core tiling splits M over several CTAs (a fused kernel would repeat the gather
+// and the tree walks once per M slice).
+static bool use_pipe(itlumm_plan P) {
+  if (!P->tc.ok) return false;
+  if (P->algo == ITLUMM_ALGO_TC_PIPE) return true;
+  return P->algo == ITLUMM_ALGO_AUTO && P->tc.G > 1;
 }
 
 static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm_dtype dtype, int64_t lda,
@@ -374,6 +401,31 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
   return ITLUMM_OK;
 }
 
+// encode -> codes scratch (L2-resident) -> TC accumulate, chunked by the scratch height.
+static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N,
+                                 float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(P->scratch_mu);
+  if (P->scratch_used) CUDA_TRY(cudaStreamWaitEvent(s, P->scratch_ev, 0));
+  const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
+  int32_t launches = 0;
+  for (int64_t r0 = 0; r0 < N; r0 += P->scratch_rows) {
+    const int64_t rows = std::min<int64_t>(P->scratch_rows, N - r0);
+    const void* Ar = (const uint8_t*)A + (size_t)r0 * lda * es;
+    itlumm_status st = launch_encode(P, Ar, dtype, lda, rows, P->scratch, P->scratch_ldc, s);
+    if (st != ITLUMM_OK) return st;
+    TcArgs a{};
+    a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;
+    a.out = out + (size_t)r0 * ldo; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
+    st = tc_launch(P->tc, P->dp, false, false, a, s);
+    if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
+    launches += 2;
+  }
+  CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
+  P->scratch_used = true;
+  g_launches = launches;
+  return ITLUMM_OK;
+}
+
 extern "C" itlumm_status itlumm_lut_accumulate(itlumm_plan P, const uint8_t* codes, int64_t ldc, int64_t N,
                                                int32_t* acc, int64_t ldacc, float* out, int64_t ldo,
                                                itlumm_epilogue epi, void* stream) {
@@ -403,6 +455,7 @@ extern "C" itlumm_status itlumm_amm(itlumm_plan P, const void* A, itlumm_dtype d
   if (N == 0) return ITLUMM_OK;
   if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
   DeviceGuard dg(P->device);
+  if (use_pipe(P)) return launch_pipe(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
   return launch_lut(P, true, A, dtype, lda, nullptr, 0, N, nullptr, 0, out, ldo, epi, (cudaStream_t)stream);
 }
 
@@ -444,9 +497,13 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
     float* dO = (float*)(dA + in_b);
     CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, (const uint8_t*)A_host + (size_t)r0 * lda * es, (size_t)lda * es,
                                row_in, rows, cudaMemcpyHostToDevice, s));
-    st = launch_lut(P, true, dA, dtype, P->D, nullptr, 0, rows, nullptr, 0, dO, P->M, epi, s);
+    if (use_pipe(P)) {
+      st = launch_pipe(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
+    } else {
+      st = launch_lut(P, true, dA, dtype, P->D, nullptr, 0, rows, nullptr, 0, dO, P->M, epi, s);
+    }
     if (st != ITLUMM_OK) return st;
-    launches += 1;
+    launches += g_launches;
     CUDA_TRY(cudaMemcpy2DAsync(out_host + (size_t)r0 * ldo, (size_t)ldo * 4, dO, row_out, row_out, rows,
                                cudaMemcpyDeviceToHost, s));
   }

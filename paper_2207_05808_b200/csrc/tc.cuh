@@ -26,12 +26,15 @@ namespace itlumm {
 constexpr int kTcProducerWarps = 4;
 constexpr int kTcProducers = 32 * kTcProducerWarps;           // one producer thread per tile row
 constexpr int kTcMmaWarp = kTcProducerWarps;                   // warp 4
-constexpr int kTcEpiWarp0 = kTcProducerWarps + 1;              // warps 5..8
-constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + 4);    // 288
+constexpr int kTcEpiWarp0 = kTcProducerWarps + 1;              // warps 5..12
+constexpr int kTcEpiWarps = 8;                                 // 2 per TMEM lane quadrant
+constexpr int kTcEpiThreads = 32 * kTcEpiWarps;
+constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + kTcEpiWarps);   // 416
 constexpr int kTcRows = 128;                                   // UMMA M
 constexpr int kKBlock = 128;                                   // bytes of K per block = 8 codebooks
-constexpr int kTcStages = 4;                                   // A ring depth (K-blocks)
-constexpr size_t kTcBBudget = 144 * 1024;                      // resident LUT slice budget
+constexpr int kTcStages = 3;                                   // A ring depth (K-blocks)
+constexpr size_t kTcBBudget = 128 * 1024;                      // resident LUT slice budget
+constexpr int kTcStage = 32 * 32 * 4;                          // epilogue staging per warp (bytes)
 
 struct TcPlan {
   bool ok = false;
@@ -125,13 +128,14 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t j) {
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
 struct TcSmem {
-  size_t b, a, thr, cols, sc, ot, bar, tmem, total;
+  size_t b, a, stg, thr, cols, sc, ot, bar, tmem, total;
 };
 __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS) {
   TcSmem s{};
   size_t o = 0;
   s.b = o;    o += (size_t)KB * NS * kKBlock;
   s.a = o;    o += (size_t)kTcStages * kTcRows * kKBlock;
+  s.stg = o;  o += (size_t)kTcEpiWarps * kTcStage;
   s.thr = o;  o += (size_t)C * 16 * 4;          // thresholds [C][16] (15 used)
   s.cols = o; o += (size_t)C * 16;              // cols [C][4]
   s.sc = o;   o += (size_t)NS * 4;
@@ -145,8 +149,9 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS) {
 
 template <bool FUSED, typename T>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // align in the shared window without leaving the shared address space (keeps LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
   const TcSmem L = tc_smem_layout(C, KB, NS);
   uint8_t* b_s = smem + L.b;
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
     }
     if (threadIdx.x == 0) {
       for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers); mbar_init(empty_bar + s, 1); }
-      for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, 128); }
+      for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kTcMmaWarp) {
@@ -205,66 +210,90 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
 
   if (warp < kTcProducerWarps) {
     // ============================================================== producers: one row each
+    // The input of K-block i+1 (32 gathered values, or 4 code bytes) is loaded before K-block i
+    // is encoded and written, so one K-block of loads is always in flight per thread.
     const int r = threadIdx.x;                       // row within the tile, 0..127
+    const bool codes_u32 = !FUSED && ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.codes) & 3) == 0);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    float vc[8][4], vn[8][4];
+    uint32_t cc = 0, cn = 0;
+    auto load = [&](int64_t tile, int kb, float (&v)[8][4], uint32_t& cw) {
       const int64_t row = tile * kTcRows + r;
-      const bool valid = row < g.N;
-      const T* a = FUSED ? reinterpret_cast<const T*>(g.A) + (valid ? row : 0) * g.lda : nullptr;
-      for (int kb = 0; kb < KB; ++kb) {
-        // codes of codebooks 8kb .. 8kb+7 of this row
-        uint32_t code[8];
-        if (FUSED) {
-          float v[8][4];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = kb * 8 + j;
-            if (valid && c < C) {
-              const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
-              v[j][0] = InTraits<T>::load(a + col.x);
-              v[j][1] = InTraits<T>::load(a + col.y);
-              v[j][2] = InTraits<T>::load(a + col.z);
-              v[j][3] = InTraits<T>::load(a + col.w);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = kb * 8 + j;
-            code[j] = 16;                             // 16 = no one-hot bit (padding)
-            if (valid && c < C) {
-              const float* th = thr_s + c * 16;
-              int node = 0;
-#pragma unroll
-              for (int t = 0; t < kLevels; ++t) node = 2 * node + (v[j][t] > th[(1 << t) - 1 + node] ? 1 : 0);
-              code[j] = (uint32_t)node;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = kb * 8 + j;
-            code[j] = 16;
-            if (valid && c < C) {
-              const uint32_t byte = g.codes[row * g.ldc + (c >> 1)];
-              code[j] = (c & 1) ? (byte >> 4) : (byte & 15u);
-            }
-          }
-        }
-        mbar_wait(empty_bar + stage, phase ^ 1);      // MMA finished reading this stage
-        uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
+      if (row >= g.N) return;
+      if (FUSED) {
+        const T* a = reinterpret_cast<const T*>(g.A) + row * g.lda;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t k = code[j];
-          const uint32_t bit = (k < 16) ? (1u << ((k & 3u) * 8u)) : 0u;
-          const uint32_t w = k >> 2;
-          const uint4 oh = make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
-          *reinterpret_cast<uint4*>(st + sw128_off(r, j)) = oh;
+          const int c = kb * 8 + j;
+          if (c < C) {
+            const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+            v[j][0] = InTraits<T>::load(a + col.x);
+            v[j][1] = InTraits<T>::load(a + col.y);
+            v[j][2] = InTraits<T>::load(a + col.z);
+            v[j][3] = InTraits<T>::load(a + col.w);
+          }
         }
-        fence_proxy_async_smem();
-        mbar_arrive(full_bar + stage);
-        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      } else {
+        const uint8_t* cp = g.codes + row * g.ldc + kb * 4;
+        const int nbytes = ((C + 1) >> 1) - kb * 4;      // valid code bytes from this K-block
+        if (codes_u32 && nbytes >= 4) {
+          cw = __ldg(reinterpret_cast<const unsigned int*>(cp));
+        } else {
+          cw = 0;
+          for (int b = 0; b < 4 && b < nbytes; ++b) cw |= (uint32_t)__ldg(cp + b) << (8 * b);
+        }
       }
+    };
+    int64_t tile = group;
+    int kb = 0;
+    if (tile < ntiles) load(tile, 0, vc, cc);
+    while (tile < ntiles) {
+      int64_t ntile = tile;
+      int nkb = kb + 1;
+      if (nkb == KB) { nkb = 0; ntile += ngroups; }
+      if (ntile < ntiles) load(ntile, nkb, vn, cn);
+      const bool valid = tile * kTcRows + r < g.N;
+      uint32_t code[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = kb * 8 + j;
+        code[j] = 16;                                   // 16 = no one-hot bit (padding)
+        if (valid && c < C) {
+          if (FUSED) {
+            const float* th = thr_s + c * 16;
+            int node = 0;
+#pragma unroll
+            for (int t = 0; t < kLevels; ++t) node = 2 * node + (vc[j][t] > th[(1 << t) - 1 + node] ? 1 : 0);
+            code[j] = (uint32_t)node;
+          } else {
+            code[j] = (cc >> (4 * j)) & 15u;
+          }
+        }
+      }
+      mbar_wait(empty_bar + stage, phase ^ 1);        // MMA finished reading this stage
+      uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t k = code[j];
+        const uint32_t bit = (k < 16) ? (1u << ((k & 3u) * 8u)) : 0u;
+        const uint32_t w = k >> 2;
+        const uint4 oh = make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
+        *reinterpret_cast<uint4*>(st + sw128_off(r, j)) = oh;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(full_bar + stage);
+      if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      if (FUSED) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) vc[j][t] = vn[j][t];
+      } else {
+        cc = cn;
+      }
+      tile = ntile;
+      kb = nkb;
     }
   } else if (warp == kTcMmaWarp) {
     // ============================================================== MMA issuer
@@ -296,47 +325,80 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
-    // ============================================================== epilogue: one row per thread
-    const int q = warp & 3;                           // TMEM lane quadrant of this warp
-    const int r = q * 32 + lane;                      // row within the tile
+    // ============================================================== epilogue
+    // Warp e covers TMEM lane quadrant q (rows 32q..32q+31) and every other 32-column chunk.
+    // s32 accumulators -> fp32 y (one fmaf) -> swizzled staging -> coalesced 128-byte row stores.
+    const int e = warp - kTcEpiWarp0;
+    const int q = warp & 3;
+    const int h = e >> 2;
+    const int r = q * 32 + lane;                      // this thread's row within the tile
+    uint8_t* stg = smem + L.stg + (size_t)e * kTcStage;
+    const bool out_vec = g.out && ((reinterpret_cast<uintptr_t>(g.out) & 15) == 0) && ((g.ldo & 3) == 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = group; tile < ntiles; tile += ngroups) {
       mbar_wait(accf_bar + acc, acc_phase);
       tc_fence_after();
-      const int64_t row = tile * kTcRows + r;
+      const int64_t row0 = tile * kTcRows + q * 32;   // first row of this warp's quadrant
+      const int64_t row = row0 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
-      for (int j0 = 0; j0 < NS; j0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tbase + j0, v);
+      for (int j0 = h * 32; j0 < NS; j0 += 64) {
+        const int nc = (NS - j0) >= 32 ? 32 : 16;    // columns in this chunk
+        uint32_t v[32];
+        tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        if (nc == 32) tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
         tmem_wait_ld();
-        if (row < g.N) {
-          const int mb = m0 + j0;
-          if (g.out) {
-            float y[16];
+        if (g.acc && row < g.N) {
+          int32_t* a = g.acc + row * g.ldacc + m0 + j0;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              y[j] = fmaf(sc_s[j0 + j], __uint2float_rn(v[j]), ot_s[j0 + j]);   // a4 (R8)
-              if (g.relu) y[j] = relu_pos0(y[j]);
-            }
-            float* o = g.out + row * g.ldo + mb;
-            const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (mb + 16 <= p.M);
-            if (vec) {
+          for (int j = 0; j < 32; ++j)
+            if (j < nc && m0 + j0 + j < p.M) a[j] = (int32_t)v[j];
+        }
+        if (!g.out) continue;
+        float y[32];
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) st_cs_f4(o + j, y[j], y[j + 1], y[j + 2], y[j + 3]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (mb + j < p.M) o[j] = y[j];
-            }
-          }
-          if (g.acc) {
-            int32_t* a = g.acc + row * g.ldacc + mb;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (mb + j < p.M) a[j] = (int32_t)v[j];
+        for (int j = 0; j < 32; ++j) {
+          if (j < nc) {
+            y[j] = fmaf(sc_s[j0 + j], __uint2float_rn(v[j]), ot_s[j0 + j]);   // a4, one rounding (R8)
+            if (g.relu) y[j] = relu_pos0(y[j]);
           }
         }
+        if (!out_vec) {
+          if (row < g.N) {
+            float* o = g.out + row * g.ldo + m0 + j0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nc && m0 + j0 + j < p.M) o[j] = y[j];
+          }
+          continue;
+        }
+        // stage: row `lane` owns 128 B; 16-byte chunk c stored at chunk slot c ^ (lane & 7)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (4 * c < nc)
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+        __syncwarp();
+        // store: 4 rows x 8 chunks per instruction (lane -> row i*4 + lane/8, chunk lane%8)
+        const int cq = lane & 7;
+        const int mcol = m0 + j0 + 4 * cq;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 4 + (lane >> 3);
+          const int64_t grow = row0 + rr;
+          if (4 * cq < nc && grow < g.N) {
+            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
+            float* o = g.out + grow * g.ldo + mcol;
+            if (mcol + 4 <= p.M) {
+              __stcs(reinterpret_cast<float4*>(o), val);
+            } else {
+              if (mcol + 0 < p.M) o[0] = val.x;
+              if (mcol + 1 < p.M) o[1] = val.y;
+              if (mcol + 2 < p.M) o[2] = val.z;
+            }
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(acce_bar + acc);

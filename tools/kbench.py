@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--algos", default="simt,tc")
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--only", default="encode,acc,fused")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.workload]
     n = cfg["N"] if args.rows is None else args.rows
@@ -47,11 +48,16 @@ def main():
     codes = plan.encode(A)
     s_a = 2 if bf16 else 4
     res = {"workload": args.workload, "rows": n}
-    res["encode_ms"] = timeit(lambda: plan.encode(A, codes=codes), args.iters)
+    only = args.only.split(",")
+    if "encode" in only:
+        res["encode_ms"] = timeit(lambda: plan.encode(A, codes=codes), args.iters)
     for algo in args.algos.split(","):
         try:
             plan.set_algo(algo)
-            res[f"{algo}_accumulate_ms"] = timeit(lambda: plan.lut_accumulate(codes, out=out, relu=cfg["relu"]), args.iters)
+            if "acc" in only:
+                res[f"{algo}_accumulate_ms"] = timeit(lambda: plan.lut_accumulate(codes, out=out, relu=cfg["relu"]), args.iters)
+            if "fused" not in only:
+                continue
             res[f"{algo}_fused_ms"] = timeit(lambda: plan.amm(A, out=out, relu=cfg["relu"]), args.iters)
             ab = n * (4 * cfg["C"] * s_a + 4 * cfg["M"]) + 16 * cfg["C"] * cfg["M"]
             res[f"{algo}_fused_GBps_alg"] = ab / (res[f"{algo}_fused_ms"] * 1e-3) / 1e9
