@@ -5,7 +5,7 @@ NO arithmetic of the method: no partitioning rule, no tree fit, no LUT, no quant
 no encode/accumulate/dequant.  It only draws the raw inputs a deployment would hand to the
 method: activations A (test rows and a training sample), the fixed weight matrix B, the
 stand-in permutation of D (the paper learns it, P:62/P:76/P:83; here it is a seeded
-random bijection, reading R1 in DESIGN.md), and the bias.
+random bijection, reading R21 in DESIGN.md), and the bias.
 
 Stand-ins (no dataset is in the container):
   * "mnist": U[0,1) pixels, each entry zeroed with p = 0.2          (BASELINE.json configs[0], [1])
