@@ -25,12 +25,14 @@ struct DevPlan {
 template <typename T> struct InTraits;
 template <> struct InTraits<float> {
   static __device__ __forceinline__ float load(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ float lds(const float* p) { return *p; }
 };
 // bf16 is carried as raw uint16 bit patterns; widening to fp32 is exact (reading R13).
 template <> struct InTraits<uint16_t> {
   static __device__ __forceinline__ float load(const uint16_t* p) {
     return __uint_as_float(static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(p))) << 16);
   }
+  static __device__ __forceinline__ float lds(const uint16_t* p) { return __uint_as_float(static_cast<uint32_t>(*p) << 16); }
 };
 
 // One depth-4 tree walk (a2): node <- 2*node + (v_t > thr[2^t-1+node]); NaN compares false.
@@ -61,6 +63,41 @@ __device__ __forceinline__ uint32_t odd_bytes(uint32_t w) { return __byte_perm(w
 __device__ __forceinline__ void add_fma_pipe(uint32_t& acc, uint32_t x, uint32_t one) {
   asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(x), "r"(one));
 }
+
+// ------------------------------------------------------------------------------ PTX helpers (mbarrier, bulk copy, PDL)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine, UBLKCP), completion counted on `bar` in bytes.
+// dst, src 16-byte aligned; bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// Programmatic dependent launch: wait for the preceding grid's memory to be visible / allow
+// the next grid to start its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ float relu_pos0(float y) { return y > 0.0f ? y : 0.0f; }
 

@@ -1,0 +1,124 @@
+// encode.cuh — a1+a2 streaming encode kernel (SURVEY.md §2.3 K1/K2, B200 form).
+//
+// Why stream whole rows: the 4C split columns of a row are scattered over it, and DRAM moves whole
+// lines, so a gather of 4C values already fetches ~98% of every row (ncu: 3072 of 3136 B per cfg2
+// row, profiles/r01).  Reading the rows as one sequential stream through the TMA engine
+// (cp.async.bulk -> shared memory, an mbarrier ring of S stages of R rows) reaches full HBM
+// bandwidth with one CTA per SM, and the gather then runs from shared memory.
+//
+// Per persistent CTA: thread 0 keeps S row tiles in flight; every thread waits on the stage's
+// mbarrier, gathers the 4 split values of (row, codebook) pairs from shared memory, walks the
+// depth-4 trees (thresholds resident in shared memory) and writes nibble-packed code bytes
+// (R14) with coalesced stores.  After the tile, a CTA barrier frees the stage and thread 0
+// refills it with the tile S steps ahead.
+#pragma once
+#include "common.cuh"
+
+namespace itlumm {
+
+constexpr int kEncConsumerWarps = 8;
+constexpr int kEncThreads = 32 * (1 + kEncConsumerWarps);   // warp 0: bulk-copy producer
+
+struct EncArgs {
+  const void* A;
+  int64_t lda;          // elements
+  int64_t N;
+  uint8_t* codes;
+  int64_t ldc;
+  int R;                // rows per stage
+  int S;                // stages
+  int row_bytes;        // bytes of one staged row (D * es, multiple of 16)
+  int contiguous;       // lda == D: a tile is one bulk copy
+  int pdl;              // let a dependent grid launch early (PDL)
+};
+
+// Shared-memory footprint: [S][R][row_bytes] rows | cols [C][4] | thr [15][C] | 2S mbarriers.
+__host__ __device__ inline size_t enc_smem_bytes(int C, int R, int S, int row_bytes) {
+  size_t o = (size_t)S * R * row_bytes;
+  o += (size_t)15 * C * 4 + (size_t)C * 16;
+  o = (o + 15) & ~(size_t)15;
+  o += (size_t)2 * S * 8;
+  return o;
+}
+
+// Warp 0 lane 0 keeps S row tiles in flight (full[s]: bytes landed; empty[s]: every consumer warp
+// is done with the stage).  Consumer warps take (row, 32-codebook group) units of a tile: lane l
+// walks the tree of codebook 32u+l, adjacent lanes pair their nibbles with one shuffle and the
+// even lane stores the byte.  No CTA-wide barrier in the loop: warps drift across stages freely.
+template <typename T>
+__global__ void __launch_bounds__(kEncThreads, 1) k_encode_rows(DevPlan p, EncArgs g) {
+  extern __shared__ __align__(16) uint8_t smem_enc[];
+  uint8_t* smem = smem_enc;
+  const int C = p.C, R = g.R, S = g.S, rb = g.row_bytes;
+  const int rs = rb / (int)sizeof(T);                 // staged row stride (elements)
+  uint8_t* rows_s = smem;
+  int32_t* cols_s = reinterpret_cast<int32_t*>(smem + (size_t)S * R * rb);   // 16-byte aligned
+  float* thr_s = reinterpret_cast<float*>(cols_s + 4 * C);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (((size_t)S * R * rb + (size_t)15 * C * 4 + (size_t)C * 16 + 15) & ~(size_t)15));
+  uint64_t* empty = full + S;
+  const int64_t ntiles = (g.N + R - 1) / R;
+  const char* A = reinterpret_cast<const char*>(g.A);
+  const size_t ldab = (size_t)g.lda * sizeof(T);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, kEncConsumerWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < 15 * C; i += blockDim.x) thr_s[i] = __ldg(p.thr_t + i);
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) cols_s[i] = __ldg(p.cols + i);
+  __syncthreads();
+  if (g.pdl) pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int s = k % S;
+        if (k >= S) mbar_wait(empty + s, (uint32_t)(((k / S) - 1) & 1));
+        const int64_t r0 = tile * R;
+        const int rows = (int)((g.N - r0) < R ? (g.N - r0) : R);
+        uint8_t* dst = rows_s + (size_t)s * R * rb;
+        mbar_arrive_expect_tx(full + s, (uint32_t)rows * rb);
+        if (g.contiguous) {
+          bulk_g2s(dst, A + r0 * ldab, (uint32_t)rows * rb, full + s);
+        } else {
+          for (int r = 0; r < rows; ++r) bulk_g2s(dst + (size_t)r * rb, A + (r0 + r) * ldab, rb, full + s);
+        }
+      }
+    }
+    return;
+  }
+
+  const int cw = warp - 1;
+  const int ngrp = (C + 31) >> 5;                      // 32-codebook groups per row
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = k % S;
+    mbar_wait(full + s, (uint32_t)((k / S) & 1));
+    const T* rows = reinterpret_cast<const T*>(rows_s + (size_t)s * R * rb);
+    const int64_t r0 = tile * R;
+    const int nrows = (int)((g.N - r0) < R ? (g.N - r0) : R);
+    for (int u = cw; u < nrows * ngrp; u += kEncConsumerWarps) {
+      const int r = u / ngrp, grp = u - r * ngrp;
+      const int c = grp * 32 + lane;
+      const T* a = rows + (size_t)r * rs;
+      uint32_t code = 0;
+      if (c < C) {
+        const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+        float v[4];
+        v[0] = InTraits<T>::lds(a + col.x);
+        v[1] = InTraits<T>::lds(a + col.y);
+        v[2] = InTraits<T>::lds(a + col.z);
+        v[3] = InTraits<T>::lds(a + col.w);
+        code = (uint32_t)tree_walk(v, thr_s, C, c);
+      }
+      const uint32_t hi = __shfl_down_sync(0xffffffffu, code, 1);
+      if (!(lane & 1) && c < C) g.codes[(r0 + r) * g.ldc + (c >> 1)] = (uint8_t)(code | (hi << 4));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+}
+
+}  // namespace itlumm

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -15,6 +16,7 @@
 
 #include "../../include/itlumm.h"
 #include "common.cuh"
+#include "encode.cuh"
 #include "simt.cuh"
 #include "tc.cuh"
 
@@ -249,6 +251,8 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   P->dp.offtot = (const float*)(base + o_ot);
   P->dp.D = D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
   P->tc.qt = qt.empty() ? nullptr : base + o_qt;
+  cudaFuncSetAttribute((const void*)k_encode_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   itlumm_status st = configure_simt(P);
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
@@ -323,8 +327,46 @@ static itlumm_status check_A(itlumm_plan P, const void* A, itlumm_dtype dtype, i
   return ITLUMM_OK;
 }
 
+// Streaming encode (k_encode_rows) when the rows can be bulk-copied (16-byte aligned rows whose
+// byte length is a multiple of 16) and a 2-stage ring fits in shared memory; otherwise the
+// per-thread gather kernel k_encode.
 static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda,
-                                   int64_t N, uint8_t* codes, int64_t ldc, cudaStream_t s) {
+                                   int64_t N, uint8_t* codes, int64_t ldc, cudaStream_t s, bool pdl = false) {
+  const int es = dtype == ITLUMM_BF16 ? 2 : 4;
+  const int64_t rb = (int64_t)P->D * es;
+  const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
+  if (aligned && rb <= 64 * 1024) {
+    // rows per stage: enough (row, 32-codebook group) units for every consumer warp, ~32 KB
+    // per stage, a multiple of the per-warp unit count when that stays under 64 KB
+    // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
+    // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
+    // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
+    // ITLUMM_ENC_STAGE_KB, ITLUMM_ENC_INFLIGHT_KB.
+    static const int stage_kb = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 24;
+    static const int inflight_kb = getenv("ITLUMM_ENC_INFLIGHT_KB") ? atoi(getenv("ITLUMM_ENC_INFLIGHT_KB")) : 100;
+    const int ngrp = (P->C + 31) / 32;
+    const int want = (kEncConsumerWarps + ngrp - 1) / ngrp;
+    int R = (int)std::max<int64_t>(want, ((int64_t)stage_kb * 1024) / rb);
+    if ((int64_t)((R + want - 1) / want * want) * rb <= 64 * 1024) R = (R + want - 1) / want * want;
+    if ((int64_t)R * rb > 64 * 1024) R = (int)std::max<int64_t>(1, (64 * 1024) / rb);
+    int S = (int)std::max<int64_t>(2, std::min<int64_t>(8, ((int64_t)inflight_kb * 1024 + R * rb / 2) / (R * rb)));
+    while (S >= 2 && enc_smem_bytes(P->C, R, S, (int)rb) > 200 * 1024) --S;
+    if (S >= 2) {
+      EncArgs g{};
+      g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
+      g.R = R; g.S = S; g.row_bytes = (int)rb; g.contiguous = lda == P->D; g.pdl = pdl ? 1 : 0;
+      const int64_t ntiles = (N + R - 1) / R;
+      const unsigned grid = (unsigned)std::min<int64_t>(ntiles, P->num_sms);
+      const size_t smem = enc_smem_bytes(P->C, R, S, (int)rb);
+      if (dtype == ITLUMM_F32)
+        k_encode_rows<float><<<grid, kEncThreads, smem, s>>>(P->dp, g);
+      else
+        k_encode_rows<uint16_t><<<grid, kEncThreads, smem, s>>>(P->dp, g);
+      CUDA_TRY(cudaGetLastError());
+      g_launches = 1;
+      return ITLUMM_OK;
+    }
+  }
   const int64_t nb = (P->C + 1) / 2;
   const int64_t total = N * nb;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)P->num_sms * 32);
@@ -405,23 +447,31 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
 static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N,
                                  float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(P->scratch_mu);
-  if (P->scratch_used) CUDA_TRY(cudaStreamWaitEvent(s, P->scratch_ev, 0));
+  // Calls on different streams share the plan's code scratch: order them through an event.  A
+  // stream being captured into a CUDA graph is ordered by the graph itself (an event recorded
+  // outside the capture cannot be waited on inside it).
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (P->scratch_used && !capturing) CUDA_TRY(cudaStreamWaitEvent(s, P->scratch_ev, 0));
   const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
   int32_t launches = 0;
   for (int64_t r0 = 0; r0 < N; r0 += P->scratch_rows) {
     const int64_t rows = std::min<int64_t>(P->scratch_rows, N - r0);
     const void* Ar = (const uint8_t*)A + (size_t)r0 * lda * es;
-    itlumm_status st = launch_encode(P, Ar, dtype, lda, rows, P->scratch, P->scratch_ldc, s);
+    itlumm_status st = launch_encode(P, Ar, dtype, lda, rows, P->scratch, P->scratch_ldc, s, true);
     if (st != ITLUMM_OK) return st;
     TcArgs a{};
     a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;
     a.out = out + (size_t)r0 * ldo; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
-    st = tc_launch(P->tc, P->dp, false, false, a, s);
+    st = tc_launch(P->tc, P->dp, false, false, a, s, true);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     launches += 2;
   }
-  CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
-  P->scratch_used = true;
+  if (!capturing) {
+    CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
+    P->scratch_used = true;
+  }
   g_launches = launches;
   return ITLUMM_OK;
 }

@@ -41,6 +41,7 @@ struct TcPlan {
   const char* why = "not configured";
   const uint8_t* qt = nullptr;   // device: [G][KB][NS][128] swizzled K-major LUT slices
   int C = 0, M = 0, KB = 0, NS = 0, G = 0, tmem_cols = 0;
+  int CS = 0;                    // codes ring stages (TMA path), 0 = codes path unavailable
   size_t smem = 0;
   int grid = 0;
 };
@@ -59,28 +60,10 @@ struct TcKArgs {
   int relu;
   const uint8_t* qt;
   int KB, NS, G, tmem_cols;
+  int CS;          // codes ring stages; > 0 selects the bulk-copy (TMA) codes path
+  int pdl;         // launched as a programmatic dependent of the encode kernel
 };
 
-// ------------------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -128,20 +111,22 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t j) {
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
 struct TcSmem {
-  size_t b, a, stg, thr, cols, sc, ot, bar, tmem, total;
+  size_t b, a, stg, codes, thr, cols, sc, ot, bar, tmem, total;
 };
-__host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS) {
+// CS codes stages of 128 rows x ldc_tma bytes (the TMA codes path; CS = 0 when unused).
+__host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS = 0, int ldc_tma = 0) {
   TcSmem s{};
   size_t o = 0;
   s.b = o;    o += (size_t)KB * NS * kKBlock;
   s.a = o;    o += (size_t)kTcStages * kTcRows * kKBlock;
   s.stg = o;  o += (size_t)kTcEpiWarps * kTcStage;
+  s.codes = o; o += (size_t)CS * kTcRows * ldc_tma;
   s.thr = o;  o += (size_t)C * 16 * 4;          // thresholds [C][16] (15 used)
   s.cols = o; o += (size_t)C * 16;              // cols [C][4]
   s.sc = o;   o += (size_t)NS * 4;
   s.ot = o;   o += (size_t)NS * 4;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;  o += (size_t)(2 * kTcStages + 4) * 8;
+  s.bar = o;  o += (size_t)(2 * kTcStages + 4 + CS + 1) * 8;
   s.tmem = o; o += 16;
   s.total = o + 1024;                           // slack for 1024-byte alignment of the base
   return s;
@@ -153,8 +138,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
-  const TcSmem L = tc_smem_layout(C, KB, NS);
+  const int CS = FUSED ? 0 : g.CS;
+  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc);
   uint8_t* b_s = smem + L.b;
+  uint8_t* codes_s = smem + L.codes;
   uint8_t* a_s = smem + L.a;
   float* thr_s = reinterpret_cast<float*>(smem + L.thr);
   int32_t* cols_s = reinterpret_cast<int32_t*>(smem + L.cols);
@@ -164,6 +151,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
   uint64_t* empty_bar = full_bar + kTcStages;
   uint64_t* accf_bar = empty_bar + kTcStages;
   uint64_t* acce_bar = accf_bar + 2;
+  uint64_t* codes_bar = acce_bar + 2;
+  uint64_t* b_bar = codes_bar + CS;                 // resident LUT slice landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
 
   const int slice = blockIdx.x % G;
@@ -173,12 +162,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
   const int64_t ntiles = (g.N + kTcRows - 1) / kTcRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- prologue: resident LUT slice (already swizzled in HBM), thresholds, columns, scales
+  // ---- prologue: the resident LUT slice (already swizzled in HBM) by bulk copy (TMA engine),
+  // thresholds, columns, scales by the threads; only the MMA warp waits for the slice.
   {
-    const uint4* src = reinterpret_cast<const uint4*>(g.qt + (size_t)slice * KB * NS * kKBlock);
-    uint4* dst = reinterpret_cast<uint4*>(b_s);
-    const int nv = KB * NS * kKBlock / 16;
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (threadIdx.x == 0) {
+      mbar_init(b_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint8_t* src = g.qt + (size_t)slice * KB * NS * kKBlock;
+      const uint32_t total = (uint32_t)KB * NS * kKBlock;
+      mbar_arrive_expect_tx(b_bar, total);
+      for (uint32_t o = 0; o < total; o += 32768u)
+        bulk_g2s(b_s + o, src + o, (total - o) < 32768u ? (total - o) : 32768u, b_bar);
+    }
     if (FUSED) {
       for (int i = threadIdx.x; i < C * 16; i += blockDim.x) {
         const int c = i >> 4, h = i & 15;
@@ -194,6 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
     if (threadIdx.x == 0) {
       for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers); mbar_init(empty_bar + s, 1); }
       for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
+      for (int s = 0; s < CS; ++s) mbar_init(codes_bar + s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kTcMmaWarp) {
@@ -201,18 +197,67 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
                    "r"(g.tmem_cols) : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    fence_proxy_async_smem();   // B slice written by generic stores, read by the tensor core
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
   }
   const uint32_t tmem_base = *tmem_slot;
+  // Everything above touched only plan memory; the codes (and `out`) belong to the stream
+  // order, so a programmatic dependent waits here for the encode grid to complete.
+  if (g.pdl) pdl_wait();
+
+  // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring.
+  auto issue_codes = [&](int64_t tile, int s) {
+    const int64_t r0 = tile * kTcRows;
+    const uint32_t bytes = (uint32_t)(((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows) * g.ldc);
+    mbar_arrive_expect_tx(codes_bar + s, bytes);
+    bulk_g2s(codes_s + (size_t)s * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + s);
+  };
 
   if (warp < kTcProducerWarps) {
     // ============================================================== producers: one row each
     // The input of K-block i+1 (32 gathered values, or 4 code bytes) is loaded before K-block i
     // is encoded and written, so one K-block of loads is always in flight per thread.
     const int r = threadIdx.x;                       // row within the tile, 0..127
+    if (!FUSED && CS > 0) {
+      // Codes arrive by bulk copy, CS tiles ahead; each producer thread reads its row's 4 code
+      // bytes per K-block from shared memory and writes 8 one-hot chunks.
+      if (r == 0)
+        for (int k = 0; k < CS; ++k) {
+          const int64_t t = group + (int64_t)k * ngroups;
+          if (t < ntiles) issue_codes(t, k);
+        }
+      int stage = 0, cs = 0;
+      uint32_t phase = 0, cph = 0;
+      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+        mbar_wait(codes_bar + cs, cph);
+        const bool valid = tile * kTcRows + r < g.N;
+        const uint8_t* crow = codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
+        for (int kb = 0; kb < KB; ++kb) {
+          const uint32_t cw = valid ? *reinterpret_cast<const uint32_t*>(crow + kb * 4) : 0u;
+          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
+          uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = kb * 8 + j;
+            const uint32_t k = (cw >> (4 * j)) & 15u;
+            const uint32_t bit = (valid && c < C) ? (1u << ((k & 3u) * 8u)) : 0u;
+            const uint32_t w = k >> 2;
+            *reinterpret_cast<uint4*>(st + sw128_off(r, j)) =
+                make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(full_bar + stage);
+          if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+        }
+        named_bar_sync(1, kTcProducers);               // every producer is done with stage cs
+        if (r == 0) {
+          const int64_t t = tile + (int64_t)CS * ngroups;
+          if (t < ntiles) issue_codes(t, cs);
+        }
+        if (++cs == CS) { cs = 0; cph ^= 1; }
+      }
+    } else {
     const bool codes_u32 = !FUSED && ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.codes) & 3) == 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -295,9 +340,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
       tile = ntile;
       kb = nkb;
     }
+    }
   } else if (warp == kTcMmaWarp) {
     // ============================================================== MMA issuer
     const uint32_t idesc = idesc_i8(NS);
+    mbar_wait(b_bar, 0);                             // resident LUT slice in shared memory
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -326,75 +373,98 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
     }
   } else {
     // ============================================================== epilogue
-    // Warp e covers TMEM lane quadrant q (rows 32q..32q+31) and every other 32-column chunk.
-    // s32 accumulators -> fp32 y (one fmaf) -> swizzled staging -> coalesced 128-byte row stores.
+    // Warp e covers TMEM lane quadrant q (rows 32q..32q+31) and the 32-column chunks j0 = 32h,
+    // 32h+64, ... (h = e / 4).  Per chunk: tcgen05.ld the raw s32 accumulators of its 32 rows,
+    // stage them row-major (16-byte slots XOR-swizzled by row) in shared memory, then each lane
+    // reads back 4 consecutive columns of one row, dequantises them with its register-resident
+    // scale/offtot (a4: one fmaf per element, R8; ReLU R9) and stores 16 bytes: every store
+    // instruction writes 4 full 128-byte row segments.
     const int e = warp - kTcEpiWarp0;
     const int q = warp & 3;
     const int h = e >> 2;
-    const int r = q * 32 + lane;                      // this thread's row within the tile
     uint8_t* stg = smem + L.stg + (size_t)e * kTcStage;
     const bool out_vec = g.out && ((reinterpret_cast<uintptr_t>(g.out) & 15) == 0) && ((g.ldo & 3) == 0);
+    const int cq = lane & 7;                          // 4-column group of this lane in a chunk
+    const int rsub = lane >> 3;                       // row within a 4-row store group
+    constexpr int kMaxChunks = 4;                     // NS <= 256 -> <= 4 chunks per warp
+    float scv[kMaxChunks][4], otv[kMaxChunks][4];
+#pragma unroll
+    for (int i = 0; i < kMaxChunks; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = h * 32 + i * 64 + 4 * cq + u;
+        scv[i][u] = j < NS ? sc_s[j] : 0.f;
+        otv[i][u] = j < NS ? ot_s[j] : 0.f;
+      }
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = group; tile < ntiles; tile += ngroups) {
       mbar_wait(accf_bar + acc, acc_phase);
       tc_fence_after();
       const int64_t row0 = tile * kTcRows + q * 32;   // first row of this warp's quadrant
-      const int64_t row = row0 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
-      for (int j0 = h * 32; j0 < NS; j0 += 64) {
-        const int nc = (NS - j0) >= 32 ? 32 : 16;    // columns in this chunk
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int j0 = h * 32 + i * 64;
+        if (j0 >= NS) break;
         uint32_t v[32];
         tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-        if (nc == 32) tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+        tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
         tmem_wait_ld();
-        if (g.acc && row < g.N) {
-          int32_t* a = g.acc + row * g.ldacc + m0 + j0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nc && m0 + j0 + j < p.M) a[j] = (int32_t)v[j];
-        }
-        if (!g.out) continue;
-        float y[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (j < nc) {
-            y[j] = fmaf(sc_s[j0 + j], __uint2float_rn(v[j]), ot_s[j0 + j]);   // a4, one rounding (R8)
-            if (g.relu) y[j] = relu_pos0(y[j]);
-          }
-        }
-        if (!out_vec) {
+        if (g.acc) {                                  // optional raw int32 output (tests)
+          const int64_t row = row0 + lane;
           if (row < g.N) {
-            float* o = g.out + row * g.ldo + m0 + j0;
+            int32_t* a = g.acc + row * g.ldacc + m0 + j0;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < nc && m0 + j0 + j < p.M) o[j] = y[j];
+              if (m0 + j0 + j < p.M) a[j] = (int32_t)v[j];
           }
-          continue;
         }
-        // stage: row `lane` owns 128 B; 16-byte chunk c stored at chunk slot c ^ (lane & 7)
+        if (!g.out) continue;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          if (4 * c < nc)
-            *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-                make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+          *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+              make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
         __syncwarp();
-        // store: 4 rows x 8 chunks per instruction (lane -> row i*4 + lane/8, chunk lane%8)
-        const int cq = lane & 7;
         const int mcol = m0 + j0 + 4 * cq;
+        if (out_vec && row0 + 32 <= g.N && m0 + j0 + 32 <= p.M) {
+          // interior chunk: no predicates, one pointer bump per 4 rows
+          float* o = g.out + (row0 + rsub) * g.ldo + mcol;
+          const int64_t step = 4 * g.ldo;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = i * 4 + (lane >> 3);
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + rsub;
+            const uint4 a4 = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
+            float y0 = fmaf(scv[i][0], __uint2float_rn(a4.x), otv[i][0]);
+            float y1 = fmaf(scv[i][1], __uint2float_rn(a4.y), otv[i][1]);
+            float y2 = fmaf(scv[i][2], __uint2float_rn(a4.z), otv[i][2]);
+            float y3 = fmaf(scv[i][3], __uint2float_rn(a4.w), otv[i][3]);
+            if (g.relu) { y0 = relu_pos0(y0); y1 = relu_pos0(y1); y2 = relu_pos0(y2); y3 = relu_pos0(y3); }
+            __stcs(reinterpret_cast<float4*>(o), make_float4(y0, y1, y2, y3));
+            o += step;
+          }
+          __syncwarp();
+          continue;
+        }
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + rsub;
           const int64_t grow = row0 + rr;
-          if (4 * cq < nc && grow < g.N) {
-            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
+          const uint4 a4 = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
+          float y0 = fmaf(scv[i][0], __uint2float_rn(a4.x), otv[i][0]);
+          float y1 = fmaf(scv[i][1], __uint2float_rn(a4.y), otv[i][1]);
+          float y2 = fmaf(scv[i][2], __uint2float_rn(a4.z), otv[i][2]);
+          float y3 = fmaf(scv[i][3], __uint2float_rn(a4.w), otv[i][3]);
+          if (g.relu) { y0 = relu_pos0(y0); y1 = relu_pos0(y1); y2 = relu_pos0(y2); y3 = relu_pos0(y3); }
+          if (grow < g.N) {
             float* o = g.out + grow * g.ldo + mcol;
-            if (mcol + 4 <= p.M) {
-              __stcs(reinterpret_cast<float4*>(o), val);
+            if (out_vec && mcol + 4 <= p.M) {
+              __stcs(reinterpret_cast<float4*>(o), make_float4(y0, y1, y2, y3));
             } else {
-              if (mcol + 0 < p.M) o[0] = val.x;
-              if (mcol + 1 < p.M) o[1] = val.y;
-              if (mcol + 2 < p.M) o[2] = val.z;
+              if (mcol + 0 < p.M) o[0] = y0;
+              if (mcol + 1 < p.M) o[1] = y1;
+              if (mcol + 2 < p.M) o[2] = y2;
+              if (mcol + 3 < p.M) o[3] = y3;
             }
           }
         }
@@ -424,13 +494,12 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   qt.clear();
   t->C = C; t->M = M;
   t->KB = (16 * C + kKBlock - 1) / kKBlock;
-  int ns_max = (int)(kTcBBudget / ((size_t)t->KB * kKBlock)) / 16 * 16;
+  int ns_max = (int)(kTcBBudget / ((size_t)t->KB * kKBlock)) / 32 * 32;
   if (ns_max > 256) ns_max = 256;
-  if (ns_max < 16) { t->ok = false; t->why = "C too large for a resident LUT slice (C > ~1150)"; return; }
+  if (ns_max < 32) { t->ok = false; t->why = "C too large for a resident LUT slice (C > ~256)"; return; }
   const int G = (M + ns_max - 1) / ns_max;
   int NS = (M + G - 1) / G;
-  NS = (NS + 15) / 16 * 16;
-  if (NS < 16) NS = 16;
+  NS = (NS + 31) / 32 * 32;                      // whole 32-column epilogue chunks
   t->G = G; t->NS = NS;
   int cols = 32;
   while (cols < 2 * NS) cols <<= 1;
@@ -458,14 +527,16 @@ inline itlumm_status tc_set_attr(size_t smem) {
   return ITLUMM_OK;
 }
 
+constexpr size_t kSmemMax = 227 * 1024;
+
 inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   if (!t.ok) return ITLUMM_OK;
   t.smem = tc_smem_layout(t.C, t.KB, t.NS).total;
-  if (t.smem > 227 * 1024) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
+  if (t.smem > kSmemMax) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
   itlumm_status st;
-  if ((st = tc_set_attr<true, float>(t.smem)) != ITLUMM_OK) return st;
-  if ((st = tc_set_attr<true, uint16_t>(t.smem)) != ITLUMM_OK) return st;
-  if ((st = tc_set_attr<false, float>(t.smem)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, float>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, uint16_t>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<false, float>(kSmemMax)) != ITLUMM_OK) return st;
   t.grid = t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
   return ITLUMM_OK;
 }
@@ -473,22 +544,46 @@ inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
 // AUTO policy: the tensor-core path when its tiling applies.
 inline bool tc_preferred(const TcPlan& t, bool simt_ok) { return t.ok || !simt_ok; }
 
+// `pdl`: launch as a programmatic dependent of the previous kernel on `s` (the encode kernel of
+// the TC_PIPE schedule): the prologue overlaps the encode's tail, the codes are read after
+// griddepcontrol.wait.
 inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, bool bf16, const TcArgs& a,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool pdl = false) {
   TcKArgs k{};
   k.A = a.A; k.lda = a.lda; k.codes = a.codes; k.ldc = a.ldc; k.N = a.N;
   k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
+  k.pdl = pdl ? 1 : 0;
+  size_t smem = t.smem;
+  k.CS = 0;
+  if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
+    // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
+    for (int cs = 4; cs >= 1; --cs) {
+      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc).total;
+      if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { k.CS = cs; smem = need; break; }
+    }
+  }
   const int64_t ntiles = (a.N + kTcRows - 1) / kTcRows;
   int64_t grid = t.grid;
   if (grid > (int64_t)t.G * ntiles) grid = (int64_t)t.G * ntiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e;
   if (fused) {
-    if (bf16) k_tc<true, uint16_t><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
-    else k_tc<true, float><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t>, dp, k);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float>, dp, k);
   } else {
-    k_tc<false, float><<<(unsigned)grid, kTcThreads, t.smem, s>>>(dp, k);
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float>, dp, k);
   }
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
   return ITLUMM_OK;
 }

@@ -14,15 +14,35 @@ import synth  # noqa: E402
 from paper_2207_05808_b200 import Plan, fit_layer  # noqa: E402
 
 
+GRAPH = True
+
+
 def timeit(fn, iters, warm=5):
+    """Mean device time per call: the calls are captured into one CUDA graph and replayed, so
+    host-side (ctypes/Python) overhead does not leak into the number."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(iters):
-        fn()
-    b.record()
+    if GRAPH:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    fn()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        g.replay()
+        b.record()
+    else:
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters
 
@@ -34,7 +54,10 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--only", default="encode,acc,fused")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
+    global GRAPH
+    GRAPH = not args.no_graph
     cfg = synth.CONFIGS[args.workload]
     n = cfg["N"] if args.rows is None else args.rows
     bf16 = cfg["dtype"] == "bf16"

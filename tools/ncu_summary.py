@@ -42,7 +42,7 @@ def main(rep, top=25):
     if len(rows) > 2:
         hh = rows[1]
         iS, iSrc, iE = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source"), hh.index("Instructions Executed")
-        dd = rows[2:]
+        dd = [r for r in rows[2:] if len(r) > iS and r[iS].replace('.', '', 1).isdigit()]
         tot = sum(float(r[iS] or 0) for r in dd) or 1
         print(f"  top stalled SASS ({tot:.0f} samples):")
         for r in sorted(dd, key=lambda r: -float(r[iS] or 0))[:top]:
