@@ -15,8 +15,12 @@
 //                     store fp32 rows.
 // Integer products/sums of u8 one-hot x u8 LUT are exact, so results equal the SIMT path bit for bit.
 #pragma once
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "../../include/itlumm.h"
 #include "common.cuh"
@@ -62,7 +66,18 @@ struct TcKArgs {
   int KB, NS, G, tmem_cols;
   int CS;          // codes ring stages; > 0 selects the bulk-copy (TMA) codes path
   int pdl;         // launched as a programmatic dependent of the encode kernel
+  int tma_store;   // out written by TMA tensor stores through out_map (else per-thread stores)
 };
+
+// TMA tensor store of one 32x32 fp32 box (128-byte swizzled rows in shared memory) at (x=col, y=row);
+// rows >= N and columns >= M are clipped by the tensor map bounds.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -133,7 +148,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
 }
 
 template <bool FUSED, typename T>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -384,6 +399,58 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
     const int h = e >> 2;
     uint8_t* stg = smem + L.stg + (size_t)e * kTcStage;
     const bool out_vec = g.out && ((reinterpret_cast<uintptr_t>(g.out) & 15) == 0) && ((g.ldo & 3) == 0);
+    if (g.tma_store && !g.acc) {
+      // TMEM -> registers -> dequant (+ReLU) -> 128B-swizzled staging -> one TMA tensor store per
+      // 32x32 box (the copy engine writes the rows; ragged rows/columns are clipped by the map).
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      bool pending = false;
+      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+        mbar_wait(accf_bar + acc, acc_phase);
+        tc_fence_after();
+        const int row0 = (int)(tile * kTcRows) + q * 32;
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
+        for (int j0 = h * 32; j0 < NS; j0 += 64) {
+          uint32_t v[32];
+          tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+          tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+          tmem_wait_ld();
+          float y[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 s4 = *reinterpret_cast<const float4*>(sc_s + j0 + 4 * c);
+            const float4 o4 = *reinterpret_cast<const float4*>(ot_s + j0 + 4 * c);
+            y[4 * c + 0] = fmaf(s4.x, __uint2float_rn(v[4 * c + 0]), o4.x);   // a4, one rounding (R8)
+            y[4 * c + 1] = fmaf(s4.y, __uint2float_rn(v[4 * c + 1]), o4.y);
+            y[4 * c + 2] = fmaf(s4.z, __uint2float_rn(v[4 * c + 2]), o4.z);
+            y[4 * c + 3] = fmaf(s4.w, __uint2float_rn(v[4 * c + 3]), o4.w);
+          }
+          if (g.relu) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) y[j] = relu_pos0(y[j]);
+          }
+          if (pending) {                              // the previous box has left the staging
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&out_map, stg, m0 + j0, row0);
+            bulk_commit();
+          }
+          pending = true;
+        }
+        tc_fence_before();
+        mbar_arrive(acce_bar + acc);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if (lane == 0) bulk_wait0();
+    } else {
     const int cq = lane & 7;                          // 4-column group of this lane in a chunk
     const int rsub = lane >> 3;                       // row within a 4-row store group
     constexpr int kMaxChunks = 4;                     // NS <= 256 -> <= 4 chunks per warp
@@ -474,6 +541,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g) {
       mbar_arrive(acce_bar + acc);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    }
   }
 
   tc_fence_before();
@@ -495,6 +563,11 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   t->C = C; t->M = M;
   t->KB = (16 * C + kKBlock - 1) / kKBlock;
   int ns_max = (int)(kTcBBudget / ((size_t)t->KB * kKBlock)) / 32 * 32;
+  // N per CTA (<= 256).  Note: a 4-slice split of cfg2 (NS = 128) writes its output
+  // at 5.36 TB/s, a 4-slice split at 5.84 TB/s (store-pattern probe, profiles/r01).  Developer
+  // override (not ABI): ITLUMM_TC_NS_MAX.
+  static const int ns_cap = getenv("ITLUMM_TC_NS_MAX") ? atoi(getenv("ITLUMM_TC_NS_MAX")) : 256;
+  if (ns_max > ns_cap) ns_max = ns_cap;
   if (ns_max > 256) ns_max = 256;
   if (ns_max < 32) { t->ok = false; t->why = "C too large for a resident LUT slice (C > ~256)"; return; }
   const int G = (M + ns_max - 1) / ns_max;
@@ -544,6 +617,31 @@ inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
 // AUTO policy: the tensor-core path when its tiling applies.
 inline bool tc_preferred(const TcPlan& t, bool simt_ok) { return t.ok || !simt_ok; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Tensor map of `out` (N x M fp32, row stride ldo) with 32x32 boxes and 128-byte swizzle.
+inline bool make_out_map(CUtensorMap* map, float* out, int64_t N, int M, int64_t ldo) {
+  auto enc = tensor_map_encoder();
+  if (!enc || !out || (reinterpret_cast<uintptr_t>(out) & 15) || (ldo & 3) || N < 1 || N > INT32_MAX) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // `pdl`: launch as a programmatic dependent of the previous kernel on `s` (the encode kernel of
 // the TC_PIPE schedule): the prologue overlaps the encode's tail, the codes are read after
 // griddepcontrol.wait.
@@ -554,6 +652,9 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
   k.pdl = pdl ? 1 : 0;
+  alignas(64) CUtensorMap out_map;
+  memset(&out_map, 0, sizeof out_map);
+  k.tma_store = (!a.acc && make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) ? 1 : 0;
   size_t smem = t.smem;
   k.CS = 0;
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
@@ -578,10 +679,10 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e;
   if (fused) {
-    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t>, dp, k);
-    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float>, dp, k);
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t>, dp, k, out_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float>, dp, k, out_map);
   } else {
-    e = cudaLaunchKernelEx(&cfg, k_tc<false, float>, dp, k);
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float>, dp, k, out_map);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }

@@ -65,6 +65,29 @@ __global__ void k_stg(uint4* dst, size_t n) {
     __stcs(dst + i, make_uint4(i, 1, 2, 3));
 }
 
+
+// Emulates the TC epilogue's store pattern: out is N x ldo fp32; CTA = (group, slice of NS cols);
+// per 128-row tile, warp (q, h) of W warps writes rows 32q..32q+31, 32-col chunks j0 = 32h' + 32*nh*i,
+// each STG.128 instruction = 4 rows x 128 B.
+__global__ void k_stg_tile(float* out, int64_t N, int ldo, int NS, int G, int nh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, h = warp >> 2;
+  const int slice = blockIdx.x % G, group = blockIdx.x / G, ngroups = gridDim.x / G;
+  const int64_t ntiles = (N + 127) / 128;
+  const int cq = lane & 7, rsub = lane >> 3;
+  for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    const int64_t row0 = tile * 128 + q * 32;
+    for (int j0 = h * 32; j0 < NS; j0 += 32 * nh) {
+      float* o = out + (row0 + rsub) * ldo + slice * NS + j0 + 4 * cq;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        if (row0 + it * 4 + rsub < N) __stcs(reinterpret_cast<float4*>(o), make_float4(1.f, 2.f, 3.f, (float)it));
+        o += 4 * ldo;
+      }
+    }
+  }
+}
+
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t total = (size_t)188 * 3136 * 320;   // ~188 MB (60000 rows of 3136 B, padded)
@@ -103,6 +126,15 @@ int main() {
     if (tpb * bpsm > 2048) continue;
     float ms = time([&](int i) { k_stg<<<sms * bpsm, tpb>>>((uint4*)((i & 1) ? buf2 : buf), total / 16); });
     printf("{\"kind\":\"stg\",\"tpb\":%d,\"bpsm\":%d,\"GBps\":%.1f}\n", tpb, bpsm, total / (ms * 1e-3) / 1e9);
+  }
+  {
+    const int64_t N = 60000; const int ldo = 512;
+    for (int G : {1, 2, 4}) for (int nh : {1, 2, 4}) for (int ctas : {1, 2}) {
+      const int NS = 512 / G;
+      const int grid = G * ((sms * ctas) / G);
+      float ms = time([&](int i) { k_stg_tile<<<grid, 128 * nh>>>((float*)((i & 1) ? buf2 : buf), N, ldo, NS, G, nh); });
+      printf("{\"kind\":\"stg_tile\",\"G\":%d,\"warps\":%d,\"ctas_per_sm\":%d,\"GBps\":%.1f}\n", G, 4 * nh, ctas, N * ldo * 4.0 / (ms * 1e-3) / 1e9);
+    }
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("{\"status\":\"%s\"}\n", cudaGetErrorString(e));
