@@ -59,10 +59,17 @@ typedef enum { ITLUMM_EPI_NONE = 0, ITLUMM_EPI_RELU = 1 } itlumm_epilogue;  /* s
  *   TC_PIPE : itlumm_amm = the encode kernel writing codes to a plan-owned, L2-resident scratch
  *             buffer, then the TC accumulate kernel (2 launches; concurrent calls on one plan
  *             are serialised on the device through an event).  itlumm_lut_accumulate = TC.
+ *   TC_SP   : itlumm_amm = ONE cooperative launch, one CTA per SM, spatially partitioned: E
+ *             CTAs encode (rows streamed by TMA) into the plan's L2-resident code buffer while
+ *             the other CTAs run the TC accumulate on codes tiles as they become ready (per-tile
+ *             ready counters; no CTA of the TC side can block an encoder).  Same serialisation of
+ *             concurrent calls as TC_PIPE.  itlumm_lut_accumulate = TC.  Falls back to TC_PIPE
+ *             where rows cannot be bulk-copied or cooperative launch is unavailable.
  * TC and TC_PIPE return EUNSUPPORTED where the tensor-core tiling does not apply.  Every
  * schedule produces bit-identical results. */
 typedef enum {
-  ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2, ITLUMM_ALGO_TC_PIPE = 3
+  ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2, ITLUMM_ALGO_TC_PIPE = 3,
+  ITLUMM_ALGO_TC_SP = 4
 } itlumm_algo;
 
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */

@@ -13,7 +13,7 @@ OK, EINVAL, ESHAPE, EUNSUPPORTED, ECUDA, ENOMEM = range(6)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA", 5: "ENOMEM"}
 F32, BF16 = 0, 1
 EPI_NONE, EPI_RELU = 0, 1
-ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3}
+ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3, "tc_sp": 4}
 
 # every symbol include/itlumm.h declares (checked by tests/test_abi.py against the header)
 EXPORTS = [

@@ -99,6 +99,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Spin (with back-off) until *p >= v, acquire at GPU scope.  Traps after ~10 s so that a broken
+// producer/consumer protocol surfaces as a launch error instead of a hung GPU.
+__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t v) {
+  uint32_t x;
+  for (uint64_t it = 0;; ++it) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    if (x >= v) return;
+    __nanosleep(it < 64 ? 32 : 256);
+    if (it > (1ull << 25)) __trap();
+  }
+}
+
 __device__ __forceinline__ float relu_pos0(float y) { return y > 0.0f ? y : 0.0f; }
 
 __device__ __forceinline__ void st_cs_f4(float* p, float a, float b, float c, float d) {

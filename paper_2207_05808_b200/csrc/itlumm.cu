@@ -19,6 +19,7 @@
 #include "encode.cuh"
 #include "simt.cuh"
 #include "tc.cuh"
+#include "sp.cuh"
 
 using namespace itlumm;
 
@@ -64,6 +65,8 @@ struct itlumm_plan_s {
   int64_t scratch_rows = 0, scratch_ldc = 0;
   cudaEvent_t scratch_ev = nullptr;
   bool scratch_used = false;
+  uint32_t* ready = nullptr;     // [scratch_rows / 128] x 2: TC_SP ready / consumed counters (zeroed)
+  bool coop = false;             // device supports cooperative launches
   // host API staging
   std::mutex host_mu;
   cudaStream_t hs[2] = {nullptr, nullptr};
@@ -224,6 +227,7 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   auto cleanup = [&](itlumm_status st) {
     if (P->dmem) cudaFree(P->dmem);
     if (P->scratch) cudaFree(P->scratch);
+    if (P->ready) cudaFree(P->ready);
     if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
     delete P;
     cudaSetDevice(prev);
@@ -262,6 +266,14 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
     P->scratch_rows = 262144;
     e = cudaMalloc(&P->scratch, (size_t)P->scratch_rows * P->scratch_ldc);
     if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "scratch cudaMalloc: %s", cudaGetErrorString(e)));
+    e = cudaMalloc(&P->ready, (size_t)P->scratch_rows / 128 * 2 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(P->ready, 0, (size_t)P->scratch_rows / 128 * 2 * sizeof(uint32_t));
+    if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "ready counters: %s", cudaGetErrorString(e)));
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cuda_device);
+    P->coop = coop != 0;
+    cudaFuncSetAttribute((const void*)k_amm_sp<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     e = cudaEventCreateWithFlags(&P->scratch_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
   }
@@ -279,6 +291,7 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
   cudaDeviceSynchronize();
   if (P->dmem) cudaFree(P->dmem);
   if (P->scratch) cudaFree(P->scratch);
+  if (P->ready) cudaFree(P->ready);
   if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
   if (P->stage) cudaFree(P->stage);
   for (auto& s : P->hs)
@@ -292,7 +305,8 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
 extern "C" itlumm_status itlumm_plan_set_algo(itlumm_plan P, itlumm_algo algo) {
   g_err.clear();
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
-  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC && algo != ITLUMM_ALGO_TC_PIPE)
+  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC && algo != ITLUMM_ALGO_TC_PIPE &&
+      algo != ITLUMM_ALGO_TC_SP)
     return fail(ITLUMM_EINVAL, "bad algo %d", (int)algo);
   P->algo = algo;
   return ITLUMM_OK;
@@ -327,6 +341,34 @@ static itlumm_status check_A(itlumm_plan P, const void* A, itlumm_dtype dtype, i
   return ITLUMM_OK;
 }
 
+// Rows per stage R and ring depth S of the streaming encoder for rows of rb bytes, or false if
+// the rows cannot be bulk-copied.  pow2: R a power of two dividing 128 (TC_SP ready counters).
+static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2, int* Rout, int* Sout) {
+  // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
+  // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
+  // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
+  // ITLUMM_ENC_STAGE_KB, ITLUMM_ENC_INFLIGHT_KB.
+  static const int stage_kb = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 24;
+  static const int inflight_kb = getenv("ITLUMM_ENC_INFLIGHT_KB") ? atoi(getenv("ITLUMM_ENC_INFLIGHT_KB")) : 100;
+  if (rb > 64 * 1024) return false;
+  const int ngrp = (P->C + 31) / 32;
+  const int want = std::min(8, (consumer_warps + ngrp - 1) / ngrp);
+  int R = (int)std::max<int64_t>(want, ((int64_t)stage_kb * 1024) / rb);
+  if ((int64_t)((R + want - 1) / want * want) * rb <= 64 * 1024) R = (R + want - 1) / want * want;
+  if ((int64_t)R * rb > 64 * 1024) R = (int)std::max<int64_t>(1, (64 * 1024) / rb);
+  if (pow2) {
+    int r2 = 1;
+    while (r2 * 2 <= R && r2 * 2 <= 128) r2 *= 2;
+    R = r2;
+  }
+  int S = (int)std::max<int64_t>(2, std::min<int64_t>(8, ((int64_t)inflight_kb * 1024 + R * rb / 2) / (R * rb)));
+  while (S >= 2 && enc_smem_bytes(P->C, R, S, (int)rb) > 200 * 1024) --S;
+  if (S < 2) return false;
+  *Rout = R;
+  *Sout = S;
+  return true;
+}
+
 // Streaming encode (k_encode_rows) when the rows can be bulk-copied (16-byte aligned rows whose
 // byte length is a multiple of 16) and a 2-stage ring fits in shared memory; otherwise the
 // per-thread gather kernel k_encode.
@@ -335,23 +377,9 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
   const int es = dtype == ITLUMM_BF16 ? 2 : 4;
   const int64_t rb = (int64_t)P->D * es;
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
-  if (aligned && rb <= 64 * 1024) {
-    // rows per stage: enough (row, 32-codebook group) units for every consumer warp, ~32 KB
-    // per stage, a multiple of the per-warp unit count when that stays under 64 KB
-    // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
-    // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
-    // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
-    // ITLUMM_ENC_STAGE_KB, ITLUMM_ENC_INFLIGHT_KB.
-    static const int stage_kb = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 24;
-    static const int inflight_kb = getenv("ITLUMM_ENC_INFLIGHT_KB") ? atoi(getenv("ITLUMM_ENC_INFLIGHT_KB")) : 100;
-    const int ngrp = (P->C + 31) / 32;
-    const int want = (kEncConsumerWarps + ngrp - 1) / ngrp;
-    int R = (int)std::max<int64_t>(want, ((int64_t)stage_kb * 1024) / rb);
-    if ((int64_t)((R + want - 1) / want * want) * rb <= 64 * 1024) R = (R + want - 1) / want * want;
-    if ((int64_t)R * rb > 64 * 1024) R = (int)std::max<int64_t>(1, (64 * 1024) / rb);
-    int S = (int)std::max<int64_t>(2, std::min<int64_t>(8, ((int64_t)inflight_kb * 1024 + R * rb / 2) / (R * rb)));
-    while (S >= 2 && enc_smem_bytes(P->C, R, S, (int)rb) > 200 * 1024) --S;
-    if (S >= 2) {
+  int R = 0, S = 0;
+  if (aligned && enc_tiling(P, rb, kEncConsumerWarps, false, &R, &S)) {
+    {
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
       g.R = R; g.S = S; g.row_bytes = (int)rb; g.contiguous = lda == P->D; g.pdl = pdl ? 1 : 0;
@@ -394,7 +422,7 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
 
 static bool use_tc(itlumm_plan P) {
   if (P->algo == ITLUMM_ALGO_SIMT) return false;
-  if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE) return true;
+  if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
   return tc_preferred(P->tc, P->simt.MS != 0);
 }
 
@@ -403,7 +431,7 @@ static bool use_tc(itlumm_plan P) {
 // and the tree walks once per M slice).
 static bool use_pipe(itlumm_plan P) {
   if (!P->tc.ok) return false;
-  if (P->algo == ITLUMM_ALGO_TC_PIPE) return true;
+  if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
   return P->algo == ITLUMM_ALGO_AUTO && P->tc.G > 1;
 }
 
@@ -476,6 +504,83 @@ static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtyp
   return ITLUMM_OK;
 }
 
+// TC_SP: one cooperative launch; E encoder CTAs + T = n*G tensor-core CTAs (see sp.cuh).
+// Returns EUNSUPPORTED (without launching) where the rows cannot be bulk-copied or the
+// cooperative grid does not fit; the caller then falls back to TC_PIPE.
+static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N,
+                               float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
+  const int es = dtype == ITLUMM_BF16 ? 2 : 4;
+  const int64_t rb = (int64_t)P->D * es;
+  const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
+  const int enc_warps = kTcThreads / 32 - 1;
+  int R = 0, S = 0;
+  if (!P->coop || !aligned || !enc_tiling(P, rb, enc_warps, true, &R, &S))
+    return fail(ITLUMM_EUNSUPPORTED, "TC_SP needs cooperative launch and 16-byte aligned rows");
+  const TcPlan& t = P->tc;
+  int CS = 0;
+  size_t smem_tc = 0;
+  for (int cs = 4; cs >= 1; --cs) {
+    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc).total;
+    if (smem_tc <= kSmemMax) { CS = cs; break; }
+  }
+  const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
+  if (CS == 0 || smem > kSmemMax) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: shared memory budget exceeded");
+  // split: encoder share ~ bytes read / (bytes read + 1.25 x bytes written) (developer override:
+  // ITLUMM_SP_ENC_CTAS)
+  static const int enc_override = getenv("ITLUMM_SP_ENC_CTAS") ? atoi(getenv("ITLUMM_SP_ENC_CTAS")) : 0;
+  const double rd = (double)P->D * es, wr = 1.25 * 4.0 * P->M;
+  int E = enc_override > 0 ? enc_override : (int)(P->num_sms * rd / (rd + wr) + 0.5);
+  int T = (P->num_sms - E) / t.G * t.G;
+  if (T < t.G) T = t.G;
+  E = P->num_sms - T;
+  if (E < 1) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: too few SMs for the split");
+  std::lock_guard<std::mutex> lk(P->scratch_mu);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (P->scratch_used && !capturing) CUDA_TRY(cudaStreamWaitEvent(s, P->scratch_ev, 0));
+  int32_t launches = 0;
+  for (int64_t r0 = 0; r0 < N; r0 += P->scratch_rows) {
+    const int64_t rows = std::min<int64_t>(P->scratch_rows, N - r0);
+    EncArgs ge{};
+    ge.A = (const uint8_t*)A + (size_t)r0 * lda * es; ge.lda = lda; ge.N = rows;
+    ge.codes = P->scratch; ge.ldc = P->scratch_ldc;
+    ge.R = R; ge.S = S; ge.row_bytes = (int)rb; ge.contiguous = lda == P->D; ge.pdl = 0;
+    TcKArgs gt{};
+    gt.codes = P->scratch; gt.ldc = P->scratch_ldc; gt.N = rows;
+    gt.out = out + (size_t)r0 * ldo; gt.ldo = ldo; gt.relu = epi == ITLUMM_EPI_RELU;
+    gt.qt = t.qt; gt.KB = t.KB; gt.NS = t.NS; gt.G = t.G; gt.tmem_cols = t.tmem_cols;
+    gt.CS = CS; gt.pdl = 0;
+    gt.ready = P->ready; gt.consumed = P->ready + P->scratch_rows / 128;
+    gt.enc_R = R; gt.enc_warps = enc_warps;
+    alignas(64) CUtensorMap out_map;
+    memset(&out_map, 0, sizeof out_map);
+    gt.tma_store = make_out_map(&out_map, gt.out, rows, P->M, ldo) ? 1 : 0;
+    SpArgs sp{E};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(E + T));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t>, P->dp, ge, gt, sp, out_map)
+                                         : cudaLaunchKernelEx(&cfg, k_amm_sp<float>, P->dp, ge, gt, sp, out_map);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ITLUMM_ECUDA, "k_amm_sp launch: %s", cudaGetErrorString(e));
+    ++launches;
+  }
+  if (!capturing) {
+    CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
+    P->scratch_used = true;
+  }
+  g_launches = launches;
+  return ITLUMM_OK;
+}
+
 extern "C" itlumm_status itlumm_lut_accumulate(itlumm_plan P, const uint8_t* codes, int64_t ldc, int64_t N,
                                                int32_t* acc, int64_t ldacc, float* out, int64_t ldo,
                                                itlumm_epilogue epi, void* stream) {
@@ -505,7 +610,14 @@ extern "C" itlumm_status itlumm_amm(itlumm_plan P, const void* A, itlumm_dtype d
   if (N == 0) return ITLUMM_OK;
   if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
   DeviceGuard dg(P->device);
-  if (use_pipe(P)) return launch_pipe(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
+  if (use_pipe(P)) {
+    if (P->algo == ITLUMM_ALGO_TC_SP) {
+      st = launch_sp(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
+      if (st != ITLUMM_EUNSUPPORTED) return st;
+      g_err.clear();
+    }
+    return launch_pipe(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
+  }
   return launch_lut(P, true, A, dtype, lda, nullptr, 0, N, nullptr, 0, out, ldo, epi, (cudaStream_t)stream);
 }
 
@@ -548,7 +660,9 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
     CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, (const uint8_t*)A_host + (size_t)r0 * lda * es, (size_t)lda * es,
                                row_in, rows, cudaMemcpyHostToDevice, s));
     if (use_pipe(P)) {
-      st = launch_pipe(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
+      st = ITLUMM_EUNSUPPORTED;
+      if (P->algo == ITLUMM_ALGO_TC_SP) st = launch_sp(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
+      if (st == ITLUMM_EUNSUPPORTED) { g_err.clear(); st = launch_pipe(P, dA, dtype, P->D, rows, dO, P->M, epi, s); }
     } else {
       st = launch_lut(P, true, dA, dtype, P->D, nullptr, 0, rows, nullptr, 0, dO, P->M, epi, s);
     }

@@ -33,7 +33,8 @@ constexpr int kTcMmaWarp = kTcProducerWarps;                   // warp 4
 constexpr int kTcEpiWarp0 = kTcProducerWarps + 1;              // warps 5..12
 constexpr int kTcEpiWarps = 8;                                 // 2 per TMEM lane quadrant
 constexpr int kTcEpiThreads = 32 * kTcEpiWarps;
-constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + kTcEpiWarps);   // 416
+constexpr int kTcLoaderWarp = kTcEpiWarp0 + kTcEpiWarps;       // warp 13: codes bulk loads
+constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + kTcEpiWarps + 1);   // 448
 constexpr int kTcRows = 128;                                   // UMMA M
 constexpr int kKBlock = 128;                                   // bytes of K per block = 8 codebooks
 constexpr int kTcStages = 3;                                   // A ring depth (K-blocks)
@@ -67,6 +68,12 @@ struct TcKArgs {
   int CS;          // codes ring stages; > 0 selects the bulk-copy (TMA) codes path
   int pdl;         // launched as a programmatic dependent of the encode kernel
   int tma_store;   // out written by TMA tensor stores through out_map (else per-thread stores)
+  // spatial pipeline (k_amm_sp): codes tile t may be loaded once ready[t] reaches
+  // ceil(rows(t) / enc_R) (one count per published encode tile); the last of the
+  // G slice CTAs to observe it resets ready[t] and consumed[t] for the next call.
+  uint32_t* ready;
+  uint32_t* consumed;
+  int enc_R, enc_warps;
 };
 
 // TMA tensor store of one 32x32 fp32 box (128-byte swizzled rows in shared memory) at (x=col, y=row);
@@ -141,15 +148,16 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
   s.sc = o;   o += (size_t)NS * 4;
   s.ot = o;   o += (size_t)NS * 4;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;  o += (size_t)(2 * kTcStages + 4 + CS + 1) * 8;
+  s.bar = o;  o += (size_t)(2 * kTcStages + 4 + 2 * CS + 1) * 8;
   s.tmem = o; o += 16;
   s.total = o + 1024;                           // slack for 1024-byte alignment of the base
   return s;
 }
 
+// One persistent CTA of the tensor-core kernel: CTA `cta` of `ncta` (slice = cta % G).
 template <bool FUSED, typename T>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+__device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const CUtensorMap* out_map,
+                                       uint8_t* smem_raw, int cta, int ncta) {
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
@@ -167,12 +175,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
   uint64_t* accf_bar = empty_bar + kTcStages;
   uint64_t* acce_bar = accf_bar + 2;
   uint64_t* codes_bar = acce_bar + 2;
-  uint64_t* b_bar = codes_bar + CS;                 // resident LUT slice landed
+  uint64_t* codes_empty = codes_bar + CS;            // producers done with a codes stage
+  uint64_t* b_bar = codes_empty + CS;                // resident LUT slice landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
 
-  const int slice = blockIdx.x % G;
-  const int group = blockIdx.x / G;
-  const int ngroups = gridDim.x / G;
+  const int slice = cta % G;
+  const int group = cta / G;
+  const int ngroups = ncta / G;
   const int m0 = slice * NS;
   const int64_t ntiles = (g.N + kTcRows - 1) / kTcRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
     if (threadIdx.x == 0) {
       for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers); mbar_init(empty_bar + s, 1); }
       for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
-      for (int s = 0; s < CS; ++s) mbar_init(codes_bar + s, 1);
+      for (int s = 0; s < CS; ++s) { mbar_init(codes_bar + s, 1); mbar_init(codes_empty + s, kTcProducers); }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kTcMmaWarp) {
@@ -221,13 +230,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
   // order, so a programmatic dependent waits here for the encode grid to complete.
   if (g.pdl) pdl_wait();
 
-  // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring.
-  auto issue_codes = [&](int64_t tile, int s) {
-    const int64_t r0 = tile * kTcRows;
-    const uint32_t bytes = (uint32_t)(((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows) * g.ldc);
-    mbar_arrive_expect_tx(codes_bar + s, bytes);
-    bulk_g2s(codes_s + (size_t)s * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + s);
-  };
+  if (warp == kTcLoaderWarp) {
+    // ============================================================== codes loader (one lane)
+    // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring; in the
+    // spatial pipeline each tile is first awaited on its ready counter.
+    if (!FUSED && CS > 0 && lane == 0) {
+      int cs = 0;
+      uint32_t cph = 0;
+      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+        mbar_wait(codes_empty + cs, cph ^ 1);
+        const int64_t r0 = tile * kTcRows;
+        const int rows = (int)((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows);
+        if (g.ready) {
+          const uint32_t need = (uint32_t)((rows + g.enc_R - 1) / g.enc_R);
+          spin_until_geq(g.ready + tile, need);
+          asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+          if (atomicAdd(g.consumed + tile, 1u) == (uint32_t)G - 1) {   // last slice to look
+            g.ready[tile] = 0u;
+            g.consumed[tile] = 0u;
+          }
+        }
+        const uint32_t bytes = (uint32_t)(rows * g.ldc);
+        mbar_arrive_expect_tx(codes_bar + cs, bytes);
+        bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
+        if (++cs == CS) { cs = 0; cph ^= 1; }
+      }
+    }
+  } else
 
   if (warp < kTcProducerWarps) {
     // ============================================================== producers: one row each
@@ -235,13 +264,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
     // is encoded and written, so one K-block of loads is always in flight per thread.
     const int r = threadIdx.x;                       // row within the tile, 0..127
     if (!FUSED && CS > 0) {
-      // Codes arrive by bulk copy, CS tiles ahead; each producer thread reads its row's 4 code
-      // bytes per K-block from shared memory and writes 8 one-hot chunks.
-      if (r == 0)
-        for (int k = 0; k < CS; ++k) {
-          const int64_t t = group + (int64_t)k * ngroups;
-          if (t < ntiles) issue_codes(t, k);
-        }
+      // Codes arrive by bulk copy (loader warp), CS tiles ahead; each producer thread reads its
+      // row's 4 code bytes per K-block from shared memory and writes 8 one-hot chunks.
       int stage = 0, cs = 0;
       uint32_t phase = 0, cph = 0;
       for (int64_t tile = group; tile < ntiles; tile += ngroups) {
@@ -265,11 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
           mbar_arrive(full_bar + stage);
           if (++stage == kTcStages) { stage = 0; phase ^= 1; }
         }
-        named_bar_sync(1, kTcProducers);               // every producer is done with stage cs
-        if (r == 0) {
-          const int64_t t = tile + (int64_t)CS * ngroups;
-          if (t < ntiles) issue_codes(t, cs);
-        }
+        mbar_arrive(codes_empty + cs);                 // this producer is done with stage cs
         if (++cs == CS) { cs = 0; cph ^= 1; }
       }
     } else {
@@ -440,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&out_map, stg, m0 + j0, row0);
+            tma_store_2d(out_map, stg, m0 + j0, row0);
             bulk_commit();
           }
           pending = true;
@@ -550,6 +570,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, cons
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(g.tmem_cols) : "memory");
   }
+}
+
+template <bool FUSED, typename T>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  tc_cta<FUSED, T>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------------------ host side

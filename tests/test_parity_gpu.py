@@ -15,7 +15,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = ATOL = 1e-6
-ALGOS = ["simt", "tc", "tc_pipe"]
+ALGOS = ["simt", "tc", "tc_pipe", "tc_sp"]
 
 
 def _plan(params, algo):

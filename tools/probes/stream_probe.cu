@@ -88,6 +88,45 @@ __global__ void k_stg_tile(float* out, int64_t N, int ldo, int NS, int G, int nh
   }
 }
 
+
+// Mixed traffic: CTAs [0, Er) stream-read `rd` bytes with bulk copies (B-byte stages, S deep);
+// the others write `wr` bytes with STG.128.  Returns when both are done.
+__global__ void k_mixed(const char* src, size_t rd, uint4* dst, size_t wr_n16, int B, int S, int Er,
+                        unsigned long long* sink) {
+  extern __shared__ __align__(16) char sm[];
+  if ((int)blockIdx.x < Er) {
+    uint64_t* bar = (uint64_t*)(sm + (size_t)S * B);
+    const size_t ntiles = rd / B;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + s)));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    auto issue = [&](size_t t, int s) {
+      asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(su32(bar + s)), "r"(B) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(su32(sm + (size_t)s * B)), "l"(src + t * B), "r"(B), "r"(su32(bar + s)) : "memory");
+    };
+    if (threadIdx.x == 0)
+      for (int k = 0; k < S; ++k) { size_t t = blockIdx.x + (size_t)k * Er; if (t < ntiles) issue(t, k); }
+    unsigned acc = 0;
+    int k = 0;
+    for (size_t t = blockIdx.x; t < ntiles; t += Er, ++k) {
+      const int s = k % S;
+      const uint32_t par = (k / S) & 1;
+      asm volatile("{.reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W;}" ::"r"(su32(bar + s)), "r"(par) : "memory");
+      acc += sm[(size_t)s * B + threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) { size_t nt = t + (size_t)S * Er; if (nt < ntiles) issue(nt, s); }
+    }
+    if (acc == 0x12345678) sink[0] = acc;
+  } else {
+    const int nw = gridDim.x - Er;
+    for (size_t i = (blockIdx.x - Er) * (size_t)blockDim.x + threadIdx.x; i < wr_n16; i += (size_t)nw * blockDim.x)
+      __stcs(dst + i, make_uint4(i, 1, 2, 3));
+  }
+}
+
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t total = (size_t)188 * 3136 * 320;   // ~188 MB (60000 rows of 3136 B, padded)
@@ -134,6 +173,14 @@ int main() {
       const int grid = G * ((sms * ctas) / G);
       float ms = time([&](int i) { k_stg_tile<<<grid, 128 * nh>>>((float*)((i & 1) ? buf2 : buf), N, ldo, NS, G, nh); });
       printf("{\"kind\":\"stg_tile\",\"G\":%d,\"warps\":%d,\"ctas_per_sm\":%d,\"GBps\":%.1f}\n", G, 4 * nh, ctas, N * ldo * 4.0 / (ms * 1e-3) / 1e9);
+    }
+  }
+  {
+    cudaFuncSetAttribute(k_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    const size_t rd = (size_t)60000 * 3136, wr = (size_t)60000 * 2048;
+    for (int Er : {60, 74, 88, 100, 148}) {
+      float ms = time([&](int i) { k_mixed<<<(Er == 148 ? 296 : sms), 256, 4 * 25088 + 128>>>((i & 1) ? buf2 : buf, rd - rd % 25088, (uint4*)((i & 1) ? buf : buf2), wr / 16, 25088, 4, Er == 148 ? 148 : Er, sink); });
+      printf("{\"kind\":\"mixed\",\"read_ctas\":%d,\"us\":%.1f,\"GBps_total\":%.1f}\n", Er, ms * 1e3, (rd + wr) / (ms * 1e-3) / 1e9);
     }
   }
   cudaError_t e = cudaDeviceSynchronize();
