@@ -133,7 +133,7 @@ itlumm_status itlumm_amm(itlumm_plan plan, const void* A, itlumm_dtype dtype, in
 
 /* Fused a1..a4 on HOST buffers (end-to-end API).  A_host: N x lda elements (pinned memory is
  * fastest; pageable works), out_host: N x ldo fp32.  Rows are streamed through plan-owned
- * device staging buffers in chunks with H2D copy / kernel / D2H copy overlapped across two
+ * device staging buffers in chunks with H2D copy / kernel / D2H copy overlapped across three
  * internal streams.  Ordered after prior work on `stream`; BLOCKING: returns when out_host is
  * written.  Staging is allocated on first use (ENOMEM possible) and kept by the plan.
  * Errors: as itlumm_amm, plus ENOMEM. */

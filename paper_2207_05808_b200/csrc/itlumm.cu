@@ -69,7 +69,7 @@ struct itlumm_plan_s {
   bool coop = false;             // device supports cooperative launches
   // host API staging
   std::mutex host_mu;
-  cudaStream_t hs[2] = {nullptr, nullptr};
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host API: 3-stage copy/compute ring
   cudaEvent_t hev = nullptr;
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -636,11 +636,13 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
   DeviceGuard dg(P->device);
   const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
   const size_t row_in = (size_t)P->D * es, row_out = (size_t)P->M * 4;
-  // chunk of rows per pipeline stage: ~32 MB of input, at least 1024 rows
-  int64_t chunk = std::max<int64_t>(1024, (int64_t)((32u << 20) / row_in));
+  // chunk of rows per pipeline stage: ~16 MB of input, at least 1024 rows; 3 stages in a ring so
+  // that the H2D of chunk i+1, the kernels of chunk i and the D2H of chunk i-1 overlap
+  constexpr int kStages = 3;
+  int64_t chunk = std::max<int64_t>(1024, (int64_t)((16u << 20) / row_in));
   chunk = std::min<int64_t>(chunk, N);
   const size_t in_b = ((size_t)chunk * row_in + 255) & ~(size_t)255, out_b = ((size_t)chunk * row_out + 255) & ~(size_t)255;
-  const size_t need = 2 * (in_b + out_b);
+  const size_t need = kStages * (in_b + out_b);
   if (P->stage_bytes < need) {
     if (P->stage) { cudaDeviceSynchronize(); cudaFree(P->stage); P->stage = nullptr; P->stage_bytes = 0; }
     if (cudaMalloc(&P->stage, need) != cudaSuccess) return fail(ITLUMM_ENOMEM, "staging cudaMalloc(%zu)", need);
@@ -654,11 +656,14 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
   int32_t launches = 0;
   for (int64_t r0 = 0, i = 0; r0 < N; r0 += chunk, ++i) {
     const int64_t rows = std::min<int64_t>(chunk, N - r0);
-    cudaStream_t s = P->hs[i & 1];
-    uint8_t* dA = (uint8_t*)P->stage + (i & 1) * (in_b + out_b);
+    cudaStream_t s = P->hs[i % kStages];
+    uint8_t* dA = (uint8_t*)P->stage + (i % kStages) * (in_b + out_b);
     float* dO = (float*)(dA + in_b);
-    CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, (const uint8_t*)A_host + (size_t)r0 * lda * es, (size_t)lda * es,
-                               row_in, rows, cudaMemcpyHostToDevice, s));
+    const uint8_t* hA = (const uint8_t*)A_host + (size_t)r0 * lda * es;
+    if ((size_t)lda * es == row_in)
+      CUDA_TRY(cudaMemcpyAsync(dA, hA, (size_t)rows * row_in, cudaMemcpyHostToDevice, s));
+    else
+      CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, hA, (size_t)lda * es, row_in, rows, cudaMemcpyHostToDevice, s));
     if (use_pipe(P)) {
       st = ITLUMM_EUNSUPPORTED;
       if (P->algo == ITLUMM_ALGO_TC_SP) st = launch_sp(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
@@ -668,8 +673,11 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
     }
     if (st != ITLUMM_OK) return st;
     launches += g_launches;
-    CUDA_TRY(cudaMemcpy2DAsync(out_host + (size_t)r0 * ldo, (size_t)ldo * 4, dO, row_out, row_out, rows,
-                               cudaMemcpyDeviceToHost, s));
+    if (ldo == P->M)
+      CUDA_TRY(cudaMemcpyAsync(out_host + (size_t)r0 * ldo, dO, (size_t)rows * row_out, cudaMemcpyDeviceToHost, s));
+    else
+      CUDA_TRY(cudaMemcpy2DAsync(out_host + (size_t)r0 * ldo, (size_t)ldo * 4, dO, row_out, row_out, rows,
+                                 cudaMemcpyDeviceToHost, s));
   }
   for (auto& s : P->hs) CUDA_TRY(cudaStreamSynchronize(s));
   g_launches = launches;
