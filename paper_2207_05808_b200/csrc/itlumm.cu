@@ -208,19 +208,20 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
     for (int h = 0; h < 15; ++h) thr_t[(size_t)h * C + c] = p->thresholds[c * 15 + h];
   std::vector<uint8_t> lut((size_t)C * 16 * Mp, 0);
   for (size_t r = 0; r < (size_t)C * 16; ++r) memcpy(&lut[r * Mp], p->lut + r * M, M);
-  std::vector<float> scale(Mp, 0.f), offtot(Mp, 0.f);
+  std::vector<uint8_t> qt;
+  tc_layout_host(C, M, p->lut, &P->tc, qt);
+  const int Mpad = std::max(Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0);   // slice columns past M read 0
+  std::vector<float> scale(Mpad, 0.f), offtot(Mpad, 0.f);
   for (int m = 0; m < M; ++m) {
     scale[m] = p->scale[m];
     const double b = p->bias ? (double)p->bias[m] : 0.0;
     offtot[m] = (float)((double)C * (double)p->offset[m] + b);   // reading R8
   }
-  std::vector<uint8_t> qt;
-  tc_layout_host(C, M, p->lut, &P->tc, qt);
 
   // one device allocation
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t o_cols = 0, o_thr = o_cols + al(cols.size() * 4), o_lut = o_thr + al(thr_t.size() * 4),
-               o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mp * 4), o_qt = o_ot + al((size_t)Mp * 4),
+               o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mpad * 4), o_qt = o_ot + al((size_t)Mpad * 4),
                total = o_qt + al(qt.size());
   int prev = 0;
   cudaGetDevice(&prev);
@@ -241,8 +242,8 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   uint8_t* base = (uint8_t*)P->dmem;
   struct { size_t off; const void* src; size_t n; } cp[] = {
       {o_cols, cols.data(), cols.size() * 4}, {o_thr, thr_t.data(), thr_t.size() * 4},
-      {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mp * 4},
-      {o_ot, offtot.data(), (size_t)Mp * 4},  {o_qt, qt.data(), qt.size()}};
+      {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mpad * 4},
+      {o_ot, offtot.data(), (size_t)Mpad * 4},  {o_qt, qt.data(), qt.size()}};
   for (auto& c : cp) {
     if (!c.n) continue;
     e = cudaMemcpy(base + c.off, c.src, c.n, cudaMemcpyHostToDevice);
@@ -272,8 +273,10 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cuda_device);
     P->coop = coop != 0;
-    cudaFuncSetAttribute((const void*)k_amm_sp<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaFuncSetAttribute((const void*)k_amm_sp<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaFuncSetAttribute((const void*)k_amm_sp<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     e = cudaEventCreateWithFlags(&P->scratch_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
   }
@@ -520,7 +523,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
   int CS = 0;
   size_t smem_tc = 0;
   for (int cs = 4; cs >= 1; --cs) {
-    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc).total;
+    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false).total;
     if (smem_tc <= kSmemMax) { CS = cs; break; }
   }
   const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
@@ -553,6 +556,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
     gt.CS = CS; gt.pdl = 0;
     gt.ready = P->ready; gt.consumed = P->ready + P->scratch_rows / 128;
     gt.enc_R = R; gt.enc_warps = enc_warps;
+    gt.stream_b = t.stream_b ? 1 : 0;
     alignas(64) CUtensorMap out_map;
     memset(&out_map, 0, sizeof out_map);
     gt.tma_store = make_out_map(&out_map, gt.out, rows, P->M, ldo) ? 1 : 0;
@@ -567,8 +571,13 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t>, P->dp, ge, gt, sp, out_map)
-                                         : cudaLaunchKernelEx(&cfg, k_amm_sp<float>, P->dp, ge, gt, sp, out_map);
+    cudaError_t e;
+    if (t.stream_b)
+      e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t, true>, P->dp, ge, gt, sp, out_map)
+                               : cudaLaunchKernelEx(&cfg, k_amm_sp<float, true>, P->dp, ge, gt, sp, out_map);
+    else
+      e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t, false>, P->dp, ge, gt, sp, out_map)
+                               : cudaLaunchKernelEx(&cfg, k_amm_sp<float, false>, P->dp, ge, gt, sp, out_map);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ITLUMM_ECUDA, "k_amm_sp launch: %s", cudaGetErrorString(e));
     ++launches;

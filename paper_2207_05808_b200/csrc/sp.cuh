@@ -20,14 +20,14 @@ struct SpArgs {
   int E;    // encoder CTAs (blockIdx < E); the remaining CTAs (a multiple of G) run tc_cta
 };
 
-template <typename T>
+template <typename T, bool SB>
 __global__ void __launch_bounds__(kTcThreads, 1) k_amm_sp(DevPlan p, EncArgs ge, TcKArgs gt, SpArgs sp,
                                                          const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_sp[];
   if ((int)blockIdx.x < sp.E) {
     enc_cta<T>(p, ge, smem_sp, blockIdx.x, sp.E, gt.ready);
   } else {
-    tc_cta<false, float>(p, gt, &out_map, smem_sp, blockIdx.x - sp.E, gridDim.x - sp.E);
+    tc_cta<false, float, SB>(p, gt, &out_map, smem_sp, blockIdx.x - sp.E, gridDim.x - sp.E);
   }
 }
 

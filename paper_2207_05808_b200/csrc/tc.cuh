@@ -40,6 +40,7 @@ constexpr int kKBlock = 128;                                   // bytes of K per
 constexpr int kTcStages = 3;                                   // A ring depth (K-blocks)
 constexpr size_t kTcBBudget = 128 * 1024;                      // resident LUT slice budget
 constexpr int kTcStage = 32 * 32 * 4;                          // epilogue staging per warp (bytes)
+constexpr size_t kSmemMax = 227 * 1024;                        // dynamic shared memory per CTA
 
 struct TcPlan {
   bool ok = false;
@@ -47,6 +48,7 @@ struct TcPlan {
   const uint8_t* qt = nullptr;   // device: [G][KB][NS][128] swizzled K-major LUT slices
   int C = 0, M = 0, KB = 0, NS = 0, G = 0, tmem_cols = 0;
   int CS = 0;                    // codes ring stages (TMA path), 0 = codes path unavailable
+  bool stream_b = false;         // LUT too large to stay resident: B K-blocks streamed per stage
   size_t smem = 0;
   int grid = 0;
 };
@@ -74,6 +76,10 @@ struct TcKArgs {
   uint32_t* ready;
   uint32_t* consumed;
   int enc_R, enc_warps;
+  // streamed-B mode (LUT larger than shared memory, codes path only): work items are
+  // (row tile, slice) pairs u = cta + k * ncta, slice = u / ntiles (consecutive CTAs share a slice,
+  // so its K-blocks stream from L2); each stage carries the one-hot K-block and the LUT K-block.
+  int stream_b;
 };
 
 // TMA tensor store of one 32x32 fp32 box (128-byte swizzled rows in shared memory) at (x=col, y=row);
@@ -136,13 +142,17 @@ struct TcSmem {
   size_t b, a, stg, codes, thr, cols, sc, ot, bar, tmem, total;
 };
 // CS codes stages of 128 rows x ldc_tma bytes (the TMA codes path; CS = 0 when unused).
-__host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS = 0, int ldc_tma = 0) {
+// stream_b: no resident slice; each of the kTcStages stages holds a one-hot K-block and a LUT
+// K-block (NS x 128 B).  fused = false: no threshold/column tables.
+__host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS = 0, int ldc_tma = 0,
+                                                 bool stream_b = false, bool fused = true) {
   TcSmem s{};
   size_t o = 0;
-  s.b = o;    o += (size_t)KB * NS * kKBlock;
+  s.b = o;    o += stream_b ? (size_t)kTcStages * NS * kKBlock : (size_t)KB * NS * kKBlock;
   s.a = o;    o += (size_t)kTcStages * kTcRows * kKBlock;
   s.stg = o;  o += (size_t)kTcEpiWarps * kTcStage;
   s.codes = o; o += (size_t)CS * kTcRows * ldc_tma;
+  if (!fused) C = 0;
   s.thr = o;  o += (size_t)C * 16 * 4;          // thresholds [C][16] (15 used)
   s.cols = o; o += (size_t)C * 16;              // cols [C][4]
   s.sc = o;   o += (size_t)NS * 4;
@@ -155,14 +165,15 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
 }
 
 // One persistent CTA of the tensor-core kernel: CTA `cta` of `ncta` (slice = cta % G).
-template <bool FUSED, typename T>
+template <bool FUSED, typename T, bool SB>
 __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const CUtensorMap* out_map,
                                        uint8_t* smem_raw, int cta, int ncta) {
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
   const int CS = FUSED ? 0 : g.CS;
-  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc);
+  static_assert(!(FUSED && SB), "the streamed-LUT mode has no fused variant");
+  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED);
   uint8_t* b_s = smem + L.b;
   uint8_t* codes_s = smem + L.codes;
   uint8_t* a_s = smem + L.a;
@@ -182,14 +193,25 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   const int slice = cta % G;
   const int group = cta / G;
   const int ngroups = ncta / G;
-  const int m0 = slice * NS;
   const int64_t ntiles = (g.N + kTcRows - 1) / kTcRows;
+  // k-th work item of this CTA: (row tile, slice); false when the CTA is done
+  auto item = [&](int64_t k, int64_t& tile, int& sl) -> bool {
+    if (SB) {
+      const int64_t u = cta + k * ncta;
+      sl = (int)(u / ntiles);
+      tile = u - (int64_t)sl * ntiles;
+      return u < ntiles * G;
+    }
+    sl = slice;
+    tile = group + k * ngroups;
+    return tile < ntiles;
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- prologue: the resident LUT slice (already swizzled in HBM) by bulk copy (TMA engine),
   // thresholds, columns, scales by the threads; only the MMA warp waits for the slice.
   {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !SB) {
       mbar_init(b_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       const uint8_t* src = g.qt + (size_t)slice * KB * NS * kKBlock;
@@ -205,13 +227,13 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       }
       for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) cols_s[i] = __ldg(p.cols + i);
     }
-    for (int i = threadIdx.x; i < NS; i += blockDim.x) {
-      const int m = m0 + i;
+    for (int i = threadIdx.x; i < NS && !SB; i += blockDim.x) {
+      const int m = slice * NS + i;
       sc_s[i] = m < p.Mp ? __ldg(p.scale + m) : 0.f;
       ot_s[i] = m < p.Mp ? __ldg(p.offtot + m) : 0.f;
     }
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers); mbar_init(empty_bar + s, 1); }
+      for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers + (SB ? 1 : 0)); mbar_init(empty_bar + s, 1); }
       for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
       for (int s = 0; s < CS; ++s) { mbar_init(codes_bar + s, 1); mbar_init(codes_empty + s, kTcProducers); }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -235,9 +257,11 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring; in the
     // spatial pipeline each tile is first awaited on its ready counter.
     if (!FUSED && CS > 0 && lane == 0) {
-      int cs = 0;
-      uint32_t cph = 0;
-      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      int cs = 0, stage = 0;
+      uint32_t cph = 0, phase = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k) {
         mbar_wait(codes_empty + cs, cph ^ 1);
         const int64_t r0 = tile * kTcRows;
         const int rows = (int)((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows);
@@ -254,6 +278,16 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         mbar_arrive_expect_tx(codes_bar + cs, bytes);
         bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
         if (++cs == CS) { cs = 0; cph ^= 1; }
+        if (SB) {                                     // this item's LUT K-blocks, one per stage
+          const uint32_t bbytes = (uint32_t)NS * kKBlock;
+          const uint8_t* src = g.qt + (size_t)sl * KB * bbytes;
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(empty_bar + stage, phase ^ 1);
+            mbar_arrive_expect_tx(full_bar + stage, bbytes);
+            bulk_g2s(b_s + (size_t)stage * bbytes, src + (size_t)kb * bbytes, bbytes, full_bar + stage);
+            if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+          }
+        }
       }
     }
   } else
@@ -268,7 +302,9 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       // row's 4 code bytes per K-block from shared memory and writes 8 one-hot chunks.
       int stage = 0, cs = 0;
       uint32_t phase = 0, cph = 0;
-      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      int64_t tile;
+      int sl;
+      for (int64_t kk = 0; item(kk, tile, sl); ++kk) {
         mbar_wait(codes_bar + cs, cph);
         const bool valid = tile * kTcRows + r < g.N;
         const uint8_t* crow = codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
@@ -379,12 +415,14 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   } else if (warp == kTcMmaWarp) {
     // ============================================================== MMA issuer
     const uint32_t idesc = idesc_i8(NS);
-    mbar_wait(b_bar, 0);                             // resident LUT slice in shared memory
+    if (!SB) mbar_wait(b_bar, 0);                    // resident LUT slice in shared memory
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    int64_t tile;
+    int sl;
+    for (int64_t k = 0; item(k, tile, sl); ++k) {
       mbar_wait(acce_bar + acc, acc_phase ^ 1);      // epilogue drained this accumulator
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(acc * NS);
@@ -393,7 +431,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kTcRows * kKBlock);
-          const uint32_t b_addr = smem_u32(b_s + (size_t)kb * NS * kKBlock);
+          const uint32_t b_addr = smem_u32(b_s + (size_t)(SB ? stage : kb) * NS * kKBlock);
 #pragma unroll
           for (int ks = 0; ks < kKBlock / 32; ++ks)
             umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
@@ -425,9 +463,14 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       int acc = 0;
       uint32_t acc_phase = 0;
       bool pending = false;
-      for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k) {
         mbar_wait(accf_bar + acc, acc_phase);
         tc_fence_after();
+        const int m0 = sl * NS;
+        const float* scp = SB ? p.scale + m0 : sc_s;   // scale/offtot of this slice's columns
+        const float* otp = SB ? p.offtot + m0 : ot_s;
         const int row0 = (int)(tile * kTcRows) + q * 32;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
         for (int j0 = h * 32; j0 < NS; j0 += 64) {
@@ -438,8 +481,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           float y[32];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 s4 = *reinterpret_cast<const float4*>(sc_s + j0 + 4 * c);
-            const float4 o4 = *reinterpret_cast<const float4*>(ot_s + j0 + 4 * c);
+            const float4 s4 = SB ? __ldg(reinterpret_cast<const float4*>(scp + j0 + 4 * c))
+                                 : *reinterpret_cast<const float4*>(scp + j0 + 4 * c);
+            const float4 o4 = SB ? __ldg(reinterpret_cast<const float4*>(otp + j0 + 4 * c))
+                                 : *reinterpret_cast<const float4*>(otp + j0 + 4 * c);
             y[4 * c + 0] = fmaf(s4.x, __uint2float_rn(v[4 * c + 0]), o4.x);   // a4, one rounding (R8)
             y[4 * c + 1] = fmaf(s4.y, __uint2float_rn(v[4 * c + 1]), o4.y);
             y[4 * c + 2] = fmaf(s4.z, __uint2float_rn(v[4 * c + 2]), o4.z);
@@ -475,19 +520,26 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     const int rsub = lane >> 3;                       // row within a 4-row store group
     constexpr int kMaxChunks = 4;                     // NS <= 256 -> <= 4 chunks per warp
     float scv[kMaxChunks][4], otv[kMaxChunks][4];
-#pragma unroll
-    for (int i = 0; i < kMaxChunks; ++i)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = h * 32 + i * 64 + 4 * cq + u;
-        scv[i][u] = j < NS ? sc_s[j] : 0.f;
-        otv[i][u] = j < NS ? ot_s[j] : 0.f;
-      }
+    int cur_sl = -1;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    int64_t tile;
+    int sl;
+    for (int64_t k = 0; item(k, tile, sl); ++k) {
       mbar_wait(accf_bar + acc, acc_phase);
       tc_fence_after();
+      const int m0 = sl * NS;
+      if (sl != cur_sl) {                             // this lane's scale/offtot, per slice
+#pragma unroll
+        for (int i = 0; i < kMaxChunks; ++i)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = h * 32 + i * 64 + 4 * cq + u;
+            scv[i][u] = j < NS ? (SB ? __ldg(p.scale + m0 + j) : sc_s[j]) : 0.f;
+            otv[i][u] = j < NS ? (SB ? __ldg(p.offtot + m0 + j) : ot_s[j]) : 0.f;
+          }
+        cur_sl = sl;
+      }
       const int64_t row0 = tile * kTcRows + q * 32;   // first row of this warp's quadrant
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
 #pragma unroll
@@ -572,10 +624,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   }
 }
 
-template <bool FUSED, typename T>
+template <bool FUSED, typename T, bool SB>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  tc_cta<FUSED, T>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
+  tc_cta<FUSED, T, SB>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -595,7 +647,19 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   static const int ns_cap = getenv("ITLUMM_TC_NS_MAX") ? atoi(getenv("ITLUMM_TC_NS_MAX")) : 256;
   if (ns_max > ns_cap) ns_max = ns_cap;
   if (ns_max > 256) ns_max = 256;
-  if (ns_max < 32) { t->ok = false; t->why = "C too large for a resident LUT slice (C > ~256)"; return; }
+  // developer override (not ABI): ITLUMM_TC_STREAM=1 streams the LUT even when it could stay resident
+  static const bool force_stream = getenv("ITLUMM_TC_STREAM") && atoi(getenv("ITLUMM_TC_STREAM")) != 0;
+  // Stream the LUT when it cannot stay resident, and also when residency would force slices
+  // narrower than the 256 columns a streamed slice gets (cfg3 C=64: 57.5 us streamed vs 72.8 us
+  // resident with 128-column slices; cfg2 C=32 keeps 256-column resident slices: 24.5 vs 31.8 us).
+  t->stream_b = ns_max < 32 || force_stream || (ns_max < 256 && M > ns_max);
+  if (!t->stream_b) {
+    // resident slice only if the fused kernel's full layout fits next to it
+    const int G0 = (M + ns_max - 1) / ns_max;
+    const int NS0 = ((M + G0 - 1) / G0 + 31) / 32 * 32;
+    if (tc_smem_layout(C, t->KB, NS0, 1, 16 * ((C + 31) / 32), false, true).total > kSmemMax) t->stream_b = true;
+  }
+  if (t->stream_b) ns_max = 256;                 // LUT K-blocks streamed per stage (large C)
   const int G = (M + ns_max - 1) / ns_max;
   int NS = (M + G - 1) / G;
   NS = (NS + 31) / 32 * 32;                      // whole 32-column epilogue chunks
@@ -619,24 +683,23 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   t->why = "";
 }
 
-template <bool FUSED, typename T>
+template <bool FUSED, typename T, bool SB>
 inline itlumm_status tc_set_attr(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc<FUSED, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc<FUSED, T, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
   return ITLUMM_OK;
 }
 
-constexpr size_t kSmemMax = 227 * 1024;
-
 inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   if (!t.ok) return ITLUMM_OK;
-  t.smem = tc_smem_layout(t.C, t.KB, t.NS).total;
+  t.smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, t.stream_b, !t.stream_b).total;
   if (t.smem > kSmemMax) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
   itlumm_status st;
-  if ((st = tc_set_attr<true, float>(kSmemMax)) != ITLUMM_OK) return st;
-  if ((st = tc_set_attr<true, uint16_t>(kSmemMax)) != ITLUMM_OK) return st;
-  if ((st = tc_set_attr<false, float>(kSmemMax)) != ITLUMM_OK) return st;
-  t.grid = t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
+  if ((st = tc_set_attr<true, float, false>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, uint16_t, false>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<false, float, false>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<false, float, true>(kSmemMax)) != ITLUMM_OK) return st;
+  t.grid = t.stream_b ? num_sms : t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
   return ITLUMM_OK;
 }
 
@@ -678,6 +741,8 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
   k.pdl = pdl ? 1 : 0;
+  k.stream_b = t.stream_b ? 1 : 0;
+  if (t.stream_b && fused) { g_tc_msg = "the LUT is streamed (too large to stay resident): no fused TC kernel"; return ITLUMM_EUNSUPPORTED; }
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
   k.tma_store = (!a.acc && make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) ? 1 : 0;
@@ -686,13 +751,14 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
     // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
     for (int cs = 4; cs >= 1; --cs) {
-      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc).total;
+      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused).total;
       if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { k.CS = cs; smem = need; break; }
     }
   }
   const int64_t ntiles = (a.N + kTcRows - 1) / kTcRows;
   int64_t grid = t.grid;
   if (grid > (int64_t)t.G * ntiles) grid = (int64_t)t.G * ntiles;
+  if (!fused && k.CS == 0 && t.stream_b) { g_tc_msg = "streamed LUT needs 16-byte aligned codes rows (ldc % 16 == 0)"; return ITLUMM_EUNSUPPORTED; }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kTcThreads);
@@ -705,10 +771,12 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e;
   if (fused) {
-    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t>, dp, k, out_map);
-    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float>, dp, k, out_map);
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false>, dp, k, out_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, false>, dp, k, out_map);
+  } else if (t.stream_b) {
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true>, dp, k, out_map);
   } else {
-    e = cudaLaunchKernelEx(&cfg, k_tc<false, float>, dp, k, out_map);
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false>, dp, k, out_map);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }

@@ -86,6 +86,8 @@ CASES = [
     (7, 129, 300, 129, 300, "f32"),       # C > 257: 16-bit SWAR lanes flushed
     (8, 1, 31, 1, 1, "f32"),
     (9, 4097, 256, 256, 64, "bf16"),
+    (10, 3000, 4096, 512, 256, "bf16"),   # cfg5-shaped: LUT K-blocks streamed (too large to stay resident)
+    (14, 700, 2048, 300, 512, "f32"),     # streamed LUT, M not a multiple of the 256-column slice
 ]
 
 
