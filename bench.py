@@ -59,7 +59,8 @@ def ncu_traffic(workload: str, algo: str):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(f"{workload}:{algo}")
+    v = d.get(f"{workload}:{algo}")
+    return v if isinstance(v, (int, float)) else None
 
 
 class ClockSampler:
