@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define ITLUMM_ABI_VERSION 1
+#define ITLUMM_ABI_VERSION 2
 
 typedef enum {
   ITLUMM_OK = 0,
@@ -140,6 +140,37 @@ itlumm_status itlumm_amm(itlumm_plan plan, const void* A, itlumm_dtype dtype, in
 itlumm_status itlumm_amm_host(itlumm_plan plan, const void* A_host, itlumm_dtype dtype,
                               int64_t lda, int64_t N, float* out_host, int64_t ldo,
                               itlumm_epilogue epi, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Whole-network chaining (BASELINE configs[3]: every linear layer of an MLP
+ * replaced by ITLUMM).  Layer l+1 consumes layer l's fp32 output.  Because a layer's
+ * encoder reads only its 4C split columns, layer l computes ONLY the (sorted, distinct) output
+ * columns layer l+1 splits on, into a compacted device buffer that layer l+1 reads through a
+ * re-mapped gather ("dead-column elimination"); the last layer computes all its columns.  The
+ * final outputs are bit-identical to running every layer in full (same LUT columns, same fmaf).
+ * --------------------------------------------------------------------------------------------- */
+typedef struct itlumm_mlp_s* itlumm_mlp; /* opaque; owns one plan per layer + intermediate buffers */
+
+/* layers[l]: host params as for itlumm_plan_create (read during the call only); requires
+ * layers[l+1].D == layers[l].M.  epis[l]: sigma of layer l (ReLU on hidden layers).
+ * Errors: as itlumm_plan_create (message prefixed with the layer index), EINVAL on a shape chain
+ * mismatch or n_layers < 1. */
+itlumm_status itlumm_mlp_create(const itlumm_params* layers, const itlumm_epilogue* epis,
+                                int32_t n_layers, int cuda_device, itlumm_mlp* out);
+
+/* Free the layers' plans and buffers (synchronises the device).  NULL is a no-op. */
+itlumm_status itlumm_mlp_destroy(itlumm_mlp mlp);
+
+/* widths[l] (host, n_layers entries, may be NULL) = output columns layer l computes. */
+itlumm_status itlumm_mlp_info(itlumm_mlp mlp, int32_t* n_layers, int32_t* widths);
+
+/* Forward pass: A device [N][lda] (dtype; lda >= layers[0].D) -> out device fp32 [N][ldo]
+ * (ldo >= last layer's M).  Rows are processed in chunks of up to 262144 through plan-owned
+ * intermediate buffers (allocated on first use: ENOMEM possible).  Async on `stream`; calls on one
+ * MLP are serialised on the device by the stream order the caller gives them.
+ * Errors: EINVAL, ENOMEM, EUNSUPPORTED, ECUDA. */
+itlumm_status itlumm_mlp_forward(itlumm_mlp mlp, const void* A, itlumm_dtype dtype, int64_t lda,
+                                 int64_t N, float* out, int64_t ldo, void* stream);
 
 /* Number of kernel launches the last successful launching call on this thread made. */
 int32_t itlumm_last_launch_count(void);

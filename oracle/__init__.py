@@ -107,3 +107,27 @@ def pack_codes(codes: np.ndarray) -> np.ndarray:
         else:
             out[:, c // 2] |= (codes[:, c] << 4).astype(np.uint8)
     return out
+
+
+def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, relus: list,
+            a_is_bf16: bool = False, nthreads: int = 8) -> list:
+    """Fit an MLP whose linear layers are all ITLUMM (BASELINE configs[3]): layer l+1
+    is fit on layer l's ITLUMM outputs of the training rows, computed by this
+    oracle's inference."""
+    X = np.asarray(A_train)
+    layers = []
+    for l, (B, C, perm, bias, relu) in enumerate(zip(Bs, Cs, perms, biases, relus)):
+        bf = a_is_bf16 and l == 0
+        p = fit.fit(X, B, C, perm, bias, a_is_bf16=bf)
+        layers.append(p)
+        if l + 1 < len(Bs):
+            X = amm(p, X, relu=relu, dtype="bf16" if bf else "f32", nthreads=nthreads)["y"]
+    return layers
+
+
+def mlp_forward(layers: list, relus: list, A: np.ndarray, a_is_bf16: bool = False, nthreads: int = 8):
+    """Every layer computed in full, output fed to the next (O9)."""
+    X = A
+    for l, (p, relu) in enumerate(zip(layers, relus)):
+        X = amm(p, X, relu=relu, dtype="bf16" if (a_is_bf16 and l == 0) else "f32", nthreads=nthreads)["y"]
+    return X

@@ -4,8 +4,8 @@
   fit_layer   — offline host fit of trees + uint8 LUT (fit-time, not the hot path)
   dist        — row sharding over ranks and the one-time parameter broadcast
 """
-from .api import Plan  # noqa: F401
-from .fit import fit_layer, chunk_bounds  # noqa: F401
+from .api import Plan, Mlp  # noqa: F401
+from .fit import fit_layer, fit_mlp, chunk_bounds  # noqa: F401
 from . import _lib  # noqa: F401
 
-__all__ = ["Plan", "fit_layer", "chunk_bounds"]
+__all__ = ["Plan", "Mlp", "fit_layer", "fit_mlp", "chunk_bounds"]

@@ -19,6 +19,7 @@ ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3, "tc_sp": 4}
 EXPORTS = [
     "itlumm_plan_create", "itlumm_plan_destroy", "itlumm_plan_set_algo", "itlumm_plan_info",
     "itlumm_encode", "itlumm_lut_accumulate", "itlumm_amm", "itlumm_amm_host",
+    "itlumm_mlp_create", "itlumm_mlp_destroy", "itlumm_mlp_info", "itlumm_mlp_forward",
     "itlumm_last_launch_count", "itlumm_last_error", "itlumm_abi_version",
 ]
 
@@ -58,6 +59,10 @@ def load():
         "itlumm_lut_accumulate": ([V, V, I64, I64, V, I64, V, I64, S, V], S),
         "itlumm_amm": ([V, V, S, I64, I64, V, I64, S, V], S),
         "itlumm_amm_host": ([V, V, S, I64, I64, V, I64, S, V], S),
+        "itlumm_mlp_create": ([V, V, I32, S, ctypes.POINTER(V)], S),
+        "itlumm_mlp_destroy": ([V], S),
+        "itlumm_mlp_info": ([V, V, V], S),
+        "itlumm_mlp_forward": ([V, V, S, I64, I64, V, I64, V], S),
         "itlumm_last_launch_count": ([], I32),
         "itlumm_last_error": ([], ctypes.c_char_p),
         "itlumm_abi_version": ([], I32),

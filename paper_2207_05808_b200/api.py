@@ -35,26 +35,33 @@ def _dtype_code(t):
     raise TypeError(f"A must be float32 or bfloat16, got {t.dtype}")
 
 
+def _params_struct(params: dict):
+    """itlumm_params for a fitted layer dict; returns (struct, arrays kept alive)."""
+    D, C, M = int(params["D"]), int(params["C"]), int(params["M"])
+    keep = dict(
+        perm=np.ascontiguousarray(params["perm"], np.int32) if params.get("perm") is not None else None,
+        boundaries=(np.ascontiguousarray(params["boundaries"], np.int32)
+                    if params.get("boundaries") is not None else None),
+        split_dim=np.ascontiguousarray(params["split_dim"], np.int32),
+        thresholds=np.ascontiguousarray(params["thresholds"], np.float32),
+        lut=np.ascontiguousarray(params["lut"], np.uint8),
+        scale=np.ascontiguousarray(params["scale"], np.float32),
+        offset=np.ascontiguousarray(params["offset"], np.float32),
+        bias=np.ascontiguousarray(params["bias"], np.float32) if params.get("bias") is not None else None,
+    )
+    p = _lib.Params(D, C, M, *[_np_ptr(keep[k]) for k in
+                               ("perm", "boundaries", "split_dim", "thresholds", "lut", "scale",
+                                "offset", "bias")])
+    return p, keep
+
+
 class Plan:
     """An immutable ITLUMM layer on one GPU (itlumm_plan)."""
 
     def __init__(self, params: dict, device: int = 0, algo: str = "auto"):
         self._lib = _lib.load()
         D, C, M = int(params["D"]), int(params["C"]), int(params["M"])
-        keep = dict(
-            perm=np.ascontiguousarray(params["perm"], np.int32) if params.get("perm") is not None else None,
-            boundaries=(np.ascontiguousarray(params["boundaries"], np.int32)
-                        if params.get("boundaries") is not None else None),
-            split_dim=np.ascontiguousarray(params["split_dim"], np.int32),
-            thresholds=np.ascontiguousarray(params["thresholds"], np.float32),
-            lut=np.ascontiguousarray(params["lut"], np.uint8),
-            scale=np.ascontiguousarray(params["scale"], np.float32),
-            offset=np.ascontiguousarray(params["offset"], np.float32),
-            bias=np.ascontiguousarray(params["bias"], np.float32) if params.get("bias") is not None else None,
-        )
-        p = _lib.Params(D, C, M, *[_np_ptr(keep[k]) for k in
-                                   ("perm", "boundaries", "split_dim", "thresholds", "lut", "scale",
-                                    "offset", "bias")])
+        p, keep = _params_struct(params)
         h = ctypes.c_void_p()
         _lib.check(self._lib.itlumm_plan_create(ctypes.byref(p), int(device), ctypes.byref(h)))
         self._h = h
@@ -128,3 +135,49 @@ class Plan:
                                              out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
                                              _stream(stream)))
         return out
+
+
+class Mlp:
+    """A chain of ITLUMM layers on one GPU (itlumm_mlp): each hidden layer computes only the output
+    columns the next layer splits on (include/itlumm.h "Whole-network chaining")."""
+
+    def __init__(self, layers: list, relus: list, device: int = 0):
+        self._lib = _lib.load()
+        structs, keeps = zip(*[_params_struct(p) for p in layers])
+        arr = (_lib.Params * len(structs))(*structs)
+        epis = (ctypes.c_int * len(relus))(*[_lib.EPI_RELU if r else _lib.EPI_NONE for r in relus])
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.itlumm_mlp_create(ctypes.cast(arr, ctypes.c_void_p), ctypes.cast(epis, ctypes.c_void_p),
+                                               len(structs), int(device), ctypes.byref(h)))
+        self._h = h
+        self.n_layers = len(structs)
+        self.D, self.M, self.device = int(layers[0]["D"]), int(layers[-1]["M"]), int(device)
+
+    def widths(self) -> list:
+        w = (ctypes.c_int32 * self.n_layers)()
+        _lib.check(self._lib.itlumm_mlp_info(self._h, None, ctypes.cast(w, ctypes.c_void_p)))
+        return list(w)
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self._lib.itlumm_last_launch_count())
+
+    def forward(self, A, out=None, stream=None):
+        N = A.shape[0]
+        if out is None:
+            out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
+        _lib.check(self._lib.itlumm_mlp_forward(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
+                                                A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
+                                                out.stride(0), _stream(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.itlumm_mlp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -146,11 +146,40 @@ static itlumm_status configure_simt(itlumm_plan_s* P) {
   return ITLUMM_OK;  // simt.MS == 0: SIMT kernels unsupported for this C (C > ~780)
 }
 
-extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_device, itlumm_plan* out) {
+// Column views used when layers are chained (itlumm_mlp): out_cols selects and orders the output
+// columns the plan computes (the only ones the next layer reads); in_map relocates the logical
+// input dims into a compacted input row of width D_in (the previous layer's selected columns).
+struct PlanView {
+  const int32_t* out_cols = nullptr;
+  int n_out = 0;
+  const int32_t* in_map = nullptr;   // [D] -> column in [0, D_in) or -1 (never a split column)
+  int D_in = 0;
+};
+
+static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, const PlanView& v,
+                                      itlumm_plan* out) {
   g_err.clear();
   if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
   *out = nullptr;
-  if (!p) return fail(ITLUMM_EINVAL, "params is NULL");
+  if (!p0) return fail(ITLUMM_EINVAL, "params is NULL");
+  // output column selection: a params copy pointing at the selected LUT columns
+  itlumm_params sel = *p0;
+  std::vector<uint8_t> lut_sel;
+  std::vector<float> sc_sel, off_sel, bias_sel;
+  if (v.out_cols) {
+    if (v.n_out < 1 || !p0->lut || !p0->scale || !p0->offset) return fail(ITLUMM_EINVAL, "bad output column selection");
+    const int Mf = p0->M, Ms = v.n_out;
+    lut_sel.resize((size_t)p0->C * 16 * Ms);
+    sc_sel.resize(Ms); off_sel.resize(Ms); bias_sel.resize(Ms);
+    for (int j = 0; j < Ms; ++j) {
+      const int m = v.out_cols[j];
+      if (m < 0 || m >= Mf) return fail(ITLUMM_EINVAL, "output column %d outside [0, %d)", m, Mf);
+      sc_sel[j] = p0->scale[m]; off_sel[j] = p0->offset[m]; bias_sel[j] = p0->bias ? p0->bias[m] : 0.f;
+      for (size_t r = 0; r < (size_t)p0->C * 16; ++r) lut_sel[r * Ms + j] = p0->lut[r * Mf + m];
+    }
+    sel.M = Ms; sel.lut = lut_sel.data(); sel.scale = sc_sel.data(); sel.offset = off_sel.data(); sel.bias = bias_sel.data();
+  }
+  const itlumm_params* p = &sel;
   const int D = p->D, C = p->C, M = p->M;
   if (D < 1 || C < 1 || M < 1) return fail(ITLUMM_EINVAL, "D, C, M must be >= 1 (got %d, %d, %d)", D, C, M);
   if (C > D) return fail(ITLUMM_EINVAL, "C (%d) > D (%d)", C, D);
@@ -187,6 +216,14 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
         return fail(ITLUMM_EINVAL, "split_dim[%d][%d] = %d outside [0, %d)", c, t, sd, bnd[c + 1] - bnd[c]);
       cols[c * 4 + t] = perm[bnd[c] + sd];   // folded gather column
     }
+  if (v.in_map) {                              // compacted input row (chained layer)
+    if (v.D_in < 1) return fail(ITLUMM_EINVAL, "bad input width");
+    for (auto& col : cols) {
+      const int m = v.in_map[col];
+      if (m < 0 || m >= v.D_in) return fail(ITLUMM_EINVAL, "split column %d missing from the compacted input", col);
+      col = m;
+    }
+  }
   for (int i = 0; i < C * 15; ++i)
     if (std::isnan(p->thresholds[i])) return fail(ITLUMM_EINVAL, "threshold %d is NaN", i);
   if (!finite_all(p->scale, M) || !finite_all(p->offset, M) || (p->bias && !finite_all(p->bias, M)))
@@ -199,7 +236,7 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   itlumm_plan_s* P = new (std::nothrow) itlumm_plan_s();
   if (!P) return fail(ITLUMM_ENOMEM, "host allocation failed");
   P->device = cuda_device;
-  P->D = D; P->C = C; P->M = M; P->Mp = (M + 15) & ~15;
+  P->D = v.in_map ? v.D_in : D; P->C = C; P->M = M; P->Mp = (M + 15) & ~15;
   const int Mp = P->Mp;
 
   // host images of the device parameters
@@ -254,7 +291,7 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   P->dp.lut = base + o_lut;
   P->dp.scale = (const float*)(base + o_sc);
   P->dp.offtot = (const float*)(base + o_ot);
-  P->dp.D = D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
+  P->dp.D = P->D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
   P->tc.qt = qt.empty() ? nullptr : base + o_qt;
   cudaFuncSetAttribute((const void*)k_encode_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -283,6 +320,10 @@ extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_dev
   cudaSetDevice(prev);
   *out = P;
   return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_create(const itlumm_params* p, int cuda_device, itlumm_plan* out) {
+  return plan_create_impl(p, cuda_device, PlanView{}, out);
 }
 
 extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
@@ -435,7 +476,8 @@ static bool use_tc(itlumm_plan P) {
 static bool use_pipe(itlumm_plan P) {
   if (!P->tc.ok) return false;
   if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
-  return P->algo == ITLUMM_ALGO_AUTO && P->tc.G > 1;
+  // a streamed LUT has no fused TC kernel: AUTO pipes it through the encoder
+  return P->algo == ITLUMM_ALGO_AUTO && (P->tc.G > 1 || P->tc.stream_b);
 }
 
 static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm_dtype dtype, int64_t lda,
@@ -689,6 +731,155 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
                                  cudaMemcpyDeviceToHost, s));
   }
   for (auto& s : P->hs) CUDA_TRY(cudaStreamSynchronize(s));
+  g_launches = launches;
+  return ITLUMM_OK;
+}
+
+// ------------------------------------------------------------------------------ MLP chaining
+struct itlumm_mlp_s {
+  int device = 0;
+  std::vector<itlumm_plan> plans;
+  std::vector<itlumm_epilogue> epis;
+  std::vector<int> width;     // output columns computed by layer l
+  std::vector<int> ld;        // row stride of layer l's intermediate buffer (width rounded up to 4)
+  std::vector<float*> buf;    // intermediate buffers, chunk rows each (all but the last layer)
+  int64_t chunk = 262144, buf_rows = 0;
+};
+
+extern "C" itlumm_status itlumm_mlp_destroy(itlumm_mlp m) {
+  g_err.clear();
+  if (!m) return ITLUMM_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(m->device);
+  cudaDeviceSynchronize();
+  for (auto* b : m->buf) if (b) cudaFree(b);
+  for (auto p : m->plans) if (p) itlumm_plan_destroy(p);
+  cudaSetDevice(prev);
+  delete m;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_mlp_create(const itlumm_params* layers, const itlumm_epilogue* epis,
+                                           int32_t n_layers, int cuda_device, itlumm_mlp* out) {
+  g_err.clear();
+  if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!layers || !epis || n_layers < 1) return fail(ITLUMM_EINVAL, "layers/epis NULL or n_layers < 1");
+  for (int l = 0; l + 1 < n_layers; ++l)
+    if (layers[l + 1].D != layers[l].M)
+      return fail(ITLUMM_EINVAL, "layer %d has D = %d but layer %d has M = %d", l + 1, layers[l + 1].D, l, layers[l].M);
+  for (int l = 0; l < n_layers; ++l)
+    if (epis[l] != ITLUMM_EPI_NONE && epis[l] != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue of layer %d", l);
+  // columns of layer l's output that layer l+1 splits on (sorted, distinct)
+  std::vector<std::vector<int32_t>> need(n_layers);
+  for (int l = 0; l + 1 < n_layers; ++l) {
+    const itlumm_params& q = layers[l + 1];
+    if (!q.split_dim || q.C < 1 || q.C > q.D) return fail(ITLUMM_EINVAL, "layer %d: bad split_dim/C", l + 1);
+    std::vector<int32_t> bnd(q.C + 1);
+    if (q.boundaries) {
+      for (int c = 0; c <= q.C; ++c) bnd[c] = q.boundaries[c];
+    } else {
+      const int qq = q.D / q.C, r = q.D % q.C;
+      bnd[0] = 0;
+      for (int c = 0; c < q.C; ++c) bnd[c + 1] = bnd[c] + qq + (c < r ? 1 : 0);
+    }
+    std::vector<char> used(q.D, 0);
+    for (int c = 0; c < q.C; ++c)
+      for (int t = 0; t < kLevels; ++t) {
+        const int sd = q.split_dim[c * 4 + t];
+        const int i = bnd[c] + sd;
+        if (sd < 0 || i < bnd[c] || i >= bnd[c + 1] || i >= q.D) return fail(ITLUMM_EINVAL, "layer %d: split_dim out of range", l + 1);
+        const int col = q.perm ? q.perm[i] : i;
+        if (col < 0 || col >= q.D) return fail(ITLUMM_EINVAL, "layer %d: bad perm", l + 1);
+        used[col] = 1;
+      }
+    for (int i = 0; i < q.D; ++i) if (used[i]) need[l].push_back(i);
+  }
+  itlumm_mlp_s* m = new (std::nothrow) itlumm_mlp_s();
+  if (!m) return fail(ITLUMM_ENOMEM, "host allocation failed");
+  m->device = cuda_device;
+  m->plans.assign(n_layers, nullptr);
+  m->epis.assign(epis, epis + n_layers);
+  m->width.assign(n_layers, 0);
+  m->ld.assign(n_layers, 0);
+  for (int l = 0; l < n_layers; ++l) {
+    PlanView v;
+    const bool last = l + 1 == n_layers;
+    if (!last) { v.out_cols = need[l].data(); v.n_out = (int)need[l].size(); }
+    std::vector<int32_t> in_map;
+    if (l > 0) {
+      in_map.assign(layers[l].D, -1);
+      for (size_t j = 0; j < need[l - 1].size(); ++j) in_map[need[l - 1][j]] = (int32_t)j;
+      v.in_map = in_map.data();
+      v.D_in = m->ld[l - 1];
+    }
+    itlumm_status st = plan_create_impl(&layers[l], cuda_device, v, &m->plans[l]);
+    if (st != ITLUMM_OK) {
+      std::string msg = "layer " + std::to_string(l) + ": " + g_err;
+      itlumm_mlp_destroy(m);
+      return fail(st, "%s", msg.c_str());
+    }
+    m->width[l] = last ? layers[l].M : (int)need[l].size();
+    m->ld[l] = (m->width[l] + 3) & ~3;        // 16-byte rows: bulk-copyable, TMA-storable
+  }
+  *out = m;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_mlp_info(itlumm_mlp m, int32_t* n_layers, int32_t* widths) {
+  g_err.clear();
+  if (!m) return fail(ITLUMM_EINVAL, "mlp is NULL");
+  if (n_layers) *n_layers = (int32_t)m->plans.size();
+  if (widths) for (size_t l = 0; l < m->plans.size(); ++l) widths[l] = m->width[l];
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_dtype dtype, int64_t lda,
+                                            int64_t N, float* out, int64_t ldo, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!m) return fail(ITLUMM_EINVAL, "mlp is NULL");
+  const int L = (int)m->plans.size();
+  itlumm_status st = check_A(m->plans[0], A, dtype, lda, N);
+  if (st != ITLUMM_OK) return st;
+  if (ldo < m->width[L - 1]) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, m->width[L - 1]);
+  if (N == 0) return ITLUMM_OK;
+  if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  DeviceGuard dg(m->device);
+  const int64_t rows_max = std::min<int64_t>(m->chunk, N);
+  if (m->buf_rows < rows_max) {
+    if (m->buf_rows) cudaDeviceSynchronize();
+    for (auto*& b : m->buf) { if (b) cudaFree(b); b = nullptr; }
+    m->buf.assign(L > 1 ? L - 1 : 0, nullptr);
+    for (int l = 0; l + 1 < L; ++l)
+      if (cudaMalloc(&m->buf[l], (size_t)rows_max * m->ld[l] * 4) != cudaSuccess) {
+        for (auto*& b : m->buf) { if (b) cudaFree(b); b = nullptr; }
+        m->buf_rows = 0;
+        return fail(ITLUMM_ENOMEM, "intermediate buffers (%lld rows)", (long long)rows_max);
+      }
+    m->buf_rows = rows_max;
+  }
+  const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
+  int32_t launches = 0;
+  for (int64_t r0 = 0; r0 < N; r0 += m->chunk) {
+    const int64_t rows = std::min<int64_t>(m->chunk, N - r0);
+    const void* in = (const uint8_t*)A + (size_t)r0 * lda * es;
+    itlumm_dtype dt = dtype;
+    int64_t ld_in = lda;
+    for (int l = 0; l < L; ++l) {
+      const bool last = l + 1 == L;
+      float* o = last ? out + (size_t)r0 * ldo : m->buf[l];
+      const int64_t ld_o = last ? ldo : m->ld[l];
+      st = itlumm_amm(m->plans[l], in, dt, ld_in, rows, o, ld_o, m->epis[l], stream);
+      if (st != ITLUMM_OK) {
+        std::string msg = "layer " + std::to_string(l) + ": " + g_err;
+        return fail(st, "%s", msg.c_str());
+      }
+      launches += g_launches;
+      in = o; dt = ITLUMM_F32; ld_in = ld_o;
+    }
+  }
   g_launches = launches;
   return ITLUMM_OK;
 }

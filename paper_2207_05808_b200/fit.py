@@ -111,3 +111,29 @@ def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | Non
     return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr,
                 lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
                 bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)))
+
+
+def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, relus: list,
+            device: int = 0, a_is_bf16: bool = False) -> list:
+    """Fit every layer of an MLP whose linear layers are all replaced by ITLUMM (BASELINE
+    configs[3]; P:110-121 incremental replacement).  Layer l+1's trees and LUT are fit on the
+    ITLUMM outputs of the training rows through the already-replaced layers 0..l (reading O9 of
+    SURVEY §8(c)); those activations come from the GPU path (Plan.amm), which is bit-identical to
+    the oracle's inference."""
+    import torch
+    from .api import Plan
+
+    X = np.asarray(A_train)
+    out = []
+    for l, (B, C, perm, bias, relu) in enumerate(zip(Bs, Cs, perms, biases, relus)):
+        p = fit_layer(X, B, C, perm, bias, a_is_bf16=(a_is_bf16 and l == 0))
+        out.append(p)
+        if l + 1 < len(Bs):
+            plan = Plan(p, device=device)
+            if a_is_bf16 and l == 0:
+                At = torch.from_numpy(np.ascontiguousarray(X).view(np.int16)).to(f"cuda:{device}").view(torch.bfloat16)
+            else:
+                At = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(f"cuda:{device}")
+            X = plan.amm(At, relu=relu).cpu().numpy()
+            plan.close()
+    return out

@@ -159,3 +159,17 @@ def small_case(seed: int, N: int, D: int, M: int, C: int, dist: str = "mnist",
         B=weights(cfg, D, M, 2.0 / D), perm=permutation(cfg, D, "seeded"),
         bias=bias(cfg, M, bias_kind),
     )
+
+
+def mlp_workload(C: int, n_rows: int, n_train: int | None = None, row0: int = 0,
+                 layers=MLP_LAYERS, cfg: int = MLP_CFG["cfg"], dist: str = MLP_CFG["dist"]) -> dict:
+    """BASELINE configs[3]: 3-layer ReLU MLP 3072-1024-1024-10, CIFAR-shaped input, one seeded
+    permutation and B ~ N(0, 2/D_in) per layer (streams 2+10l, 3+10l), bias 0, C per layer."""
+    nt = MLP_CFG["n_train"] if n_train is None else int(n_train)
+    D0 = layers[0][0]
+    return dict(
+        A=rows(dist, cfg, 0, row0, row0 + n_rows, D0), A_train=rows(dist, cfg, 1, 0, nt, D0),
+        Bs=[weights(cfg, d, m, 2.0 / d, layer=l) for l, (d, m, _) in enumerate(layers)],
+        perms=[permutation(cfg, d, "seeded", layer=l) for l, (d, _, _) in enumerate(layers)],
+        biases=[bias(cfg, m, "zero", layer=l) for l, (_, m, _) in enumerate(layers)],
+        relus=[r for (_, _, r) in layers], Cs=[int(C)] * len(layers))

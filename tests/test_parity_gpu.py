@@ -199,3 +199,47 @@ def test_error_paths_on_device():
         plan.amm(A.double())
     with pytest.raises(ItlummError):
         plan.amm(A, out=torch.empty((10, 4), device="cuda"))   # ldo < M
+
+
+def _mlp_case(C, n_rows, n_train, layers):
+    w = synth.mlp_workload(C, n_rows, n_train=n_train, layers=layers)
+    oparams = oracle.fit_mlp(w["A_train"], w["Bs"], w["Cs"], w["perms"], w["biases"], w["relus"])
+    return w, oparams
+
+
+@pytest.mark.parametrize("C,layers", [
+    (8, [(96, 64, True), (64, 48, True), (48, 10, False)]),
+    (5, [(97, 33, True), (33, 17, True), (17, 3, False)]),     # odd widths: padded compact rows
+])
+def test_mlp_chain_small(C, layers):
+    """itlumm_mlp (hidden layers compute only the columns the next layer splits on) equals the
+    oracle running every layer in full; the product fit through the GPU chain equals the oracle's
+    fit (O9) bit for bit."""
+    from paper_2207_05808_b200 import Mlp, fit_mlp
+    w, oparams = _mlp_case(C, 2500, 700, layers)
+    pparams = fit_mlp(w["A_train"], w["Bs"], w["Cs"], w["perms"], w["biases"], w["relus"])
+    for po, pp in zip(oparams, pparams):
+        for k in ("split_dim", "thresholds", "lut", "scale", "offset"):
+            assert np.array_equal(np.asarray(po[k]).view(np.uint8), np.asarray(pp[k]).view(np.uint8)), k
+    mlp = Mlp(oparams, w["relus"])
+    widths = mlp.widths()
+    assert widths[-1] == layers[-1][1] and all(widths[l] <= min(4 * C, layers[l][1]) for l in range(2))
+    y = mlp.forward(torch.from_numpy(w["A"]).cuda())
+    torch.cuda.synchronize()
+    ref = oracle.mlp_forward(oparams, w["relus"], w["A"])
+    assert_out(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("C", [16, 64])
+def test_mlp_cfg4_shapes_sampled(C):
+    """BASELINE configs[3] layer shapes 3072-1024-1024-10 (N = 70000 rows: two 65536-row seed
+    chunks, ragged tail), sampled rows against the oracle's full-layer chain."""
+    from paper_2207_05808_b200 import Mlp
+    w, oparams = _mlp_case(C, 70000, 4096, synth.MLP_LAYERS)
+    mlp = Mlp(oparams, w["relus"])
+    y = mlp.forward(torch.from_numpy(w["A"]).cuda())
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    rows = np.unique(np.concatenate([np.random.default_rng(1).choice(70000, 600, replace=False), [0, 69999]]))
+    ref = oracle.mlp_forward(oparams, w["relus"], w["A"][rows])
+    assert_out(y[rows], ref)
