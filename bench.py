@@ -34,7 +34,26 @@ WORKLOAD_DESC = {
     "cfg3_c128": "BASELINE configs[2]: CIFAR-shaped layer, N=50000 D=3072 M=1024 C=128",
     "cfg5": "BASELINE configs[4]: FFN-shaped stress case, N=262144 D=4096 M=4096 C=256, bf16 input",
 }
+for _c in synth.MLP_CFG["C_sweep"]:
+    WORKLOAD_DESC[f"cfg4_c{_c}"] = (f"BASELINE configs[3]: whole 3-layer ReLU MLP 3072-1024-1024-10, every layer "
+                                   f"ITLUMM with C={_c}, N=1048576 CIFAR-shaped rows (itlumm_mlp_forward)")
 METRIC = "fused ITLUMM rows/s"
+
+
+def _rows_chunk(a):
+    return synth.rows(*a)
+
+
+def gen_rows(dist, cfg, stream, r0, r1, D):
+    """synth.rows in parallel over the 65536-row seed chunks (identical result)."""
+    bounds = list(range(r0, r1, synth.CHUNK_ROWS)) + [r1]
+    if len(bounds) <= 3:
+        return synth.rows(dist, cfg, stream, r0, r1, D)
+    import multiprocessing as mp
+    jobs = [(dist, cfg, stream, a, b, D) for a, b in zip(bounds[:-1], bounds[1:])]
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        parts = pool.map(_rows_chunk, jobs)
+    return np.concatenate(parts, axis=0)
 
 
 def peaks():
@@ -292,6 +311,138 @@ def run_ours(args):
     return line
 
 
+def run_ours_mlp(args):
+    """BASELINE configs[3]: one step = itlumm_mlp_forward of the whole 3-layer MLP over N rows."""
+    import torch
+    import torch.distributed as dist
+    from paper_2207_05808_b200 import Mlp, fit_mlp
+    from paper_2207_05808_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    C = int(args.workload.split("_c")[1])
+    n = synth.MLP_CFG["N"] if args.rows is None else args.rows
+    layers = synth.MLP_LAYERS
+    w = synth.mlp_workload(C, 0)
+    params = None
+    if rank == 0:
+        params = fit_mlp(w["A_train"], w["Bs"], w["Cs"], w["perms"], w["biases"], w["relus"], device=local)
+    if world > 1:
+        params = [pdist.broadcast_params(params[l] if rank == 0 else None, dev) for l in range(len(layers))]
+    mlp = Mlp(params, w["relus"], device=local)
+    r0, r1 = pdist.weak_rows(n, rank)
+    A_host = gen_rows(synth.MLP_CFG["dist"], synth.MLP_CFG["cfg"], 0, r0, r1, layers[0][0])
+    A_pin = torch.from_numpy(A_host).pin_memory()
+    nbuf = 2
+    A_dev = [A_pin.to(dev) for _ in range(nbuf)]
+    M = layers[-1][1]
+    out_dev = [torch.empty((n, M), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        mlp.forward(A_dev[i % nbuf], out=out_dev[i % nbuf])
+        return mlp.last_launch_count
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(dev)
+    cs.wait_stream(stream)
+    launches = 0
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(g, stream=cs):
+            for i in range(args.steps):
+                launches += step(i)
+    stream.wait_stream(cs)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    a.record(stream)
+    g.replay()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = a.elapsed_time(b)
+    if world > 1:
+        total_ms = pdist.max_over_ranks(total_ms, dev)
+    del g
+    ms_per_step = total_ms / args.steps
+    rows_per_s = n * world / (ms_per_step * 1e-3)
+    # end to end through the public API: pinned H2D of the rows, forward, D2H of the logits
+    out_pin = torch.empty((n, M), dtype=torch.float32).pin_memory()
+    k_e2e = max(3, min(args.steps, args.e2e_steps))
+    A_e = torch.empty_like(A_dev[0])
+    o_e = torch.empty_like(out_dev[0])
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        A_e.copy_(A_pin, non_blocking=True)
+        mlp.forward(A_e, out=o_e)
+        out_pin.copy_(o_e, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / k_e2e
+    if world > 1:
+        e2e_s = pdist.max_over_ranks(e2e_s, dev)
+    widths = mlp.widths()
+    ab_row = sum(4 * C * 4 + 4 * m for (_, m, _) in layers)
+    ab = n * ab_row + sum(16 * C * m for (_, m, _) in layers)
+    peak, peak_src = peaks()
+    achieved = ab / (ms_per_step * 1e-3) / 1e9
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            cores = os.cpu_count() or 1
+            ns = 2048
+            t0 = time.perf_counter()
+            oracle.mlp_forward(params, w["relus"], A_host[:ns], nthreads=cores)
+            v = ns / (time.perf_counter() - t0)
+            cpu = {"value": v, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                   "sample": f"first {ns} rows, all 3 layers computed in full"}
+        line = {
+            "metric": METRIC, "value": rows_per_s, "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded stand-in for CIFAR-shaped rows, DESIGN.md input recipe)",
+            "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
+                       "rows_per_gpu": n, "global_rows": n * world, "layers": layers, "C": C,
+                       "computed_widths": widths, "input": "f32 row-major",
+                       "parallelism": f"rows sharded dp{world}",
+                       "l2": f"inputs larger than L2 (A {A_host.nbytes / 2**30:.1f} GiB/step), {nbuf} rotating buffers",
+                       "timing": "K steps captured as one CUDA graph, replayed once between CUDA events"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "alg_bytes_per_launch": ab, "launch_ms": ms_per_step, "peak_source": peak_src,
+                         "kernel": f"itlumm_mlp_forward ({launches // args.steps} launches per call)",
+                         "note": "algorithmic bytes of the three full layers (SURVEY 8(d): 48C + 8232 B/row); "
+                                 "hidden layers compute only the columns the next layer splits on"},
+            "e2e": {"value": n * world / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": int(A_host.nbytes),
+                    "d2h_bytes_per_step": int(n * M * 4), "api": "torch pinned copies + Mlp.forward",
+                    "steps": k_e2e},
+            "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+        }
+    mlp.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
 # --------------------------------------------------------------------------------- oracle
 def _oracle_rows_per_s(params, A, relu, dtype, nthreads):
     import oracle
@@ -322,6 +473,8 @@ def run_reference(args):
         return None
     import oracle
     from oracle import fit as ofit
+    if args.workload.startswith("cfg4"):
+        return run_reference_mlp(args)
     cfg = synth.CONFIGS[args.workload]
     n = cfg["N"] if args.rows is None else args.rows
     w0 = synth.workload(args.workload, n_rows=0)
@@ -352,6 +505,37 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_reference_mlp(args):
+    import oracle
+    C = int(args.workload.split("_c")[1])
+    n = synth.MLP_CFG["N"] if args.rows is None else args.rows
+    w = synth.mlp_workload(C, 0)
+    params = oracle.fit_mlp(w["A_train"], w["Bs"], w["Cs"], w["perms"], w["biases"], w["relus"])
+    cores = os.cpu_count() or 1
+    probe = synth.rows(synth.MLP_CFG["dist"], synth.MLP_CFG["cfg"], 0, 0, 512, synth.MLP_LAYERS[0][0])
+    t0 = time.perf_counter()
+    oracle.mlp_forward(params, w["relus"], probe, nthreads=cores)
+    rate = 512 / (time.perf_counter() - t0)
+    per_step = int(max(1, min(n, rate * args.ref_budget / max(1, args.steps + args.warmup))))
+    A = synth.rows(synth.MLP_CFG["dist"], synth.MLP_CFG["cfg"], 0, 0, per_step, synth.MLP_LAYERS[0][0])
+    for _ in range(args.warmup):
+        oracle.mlp_forward(params, w["relus"], A, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.mlp_forward(params, w["relus"], A, nthreads=cores)
+    dt = time.perf_counter() - t0
+    v = per_step * args.steps / dt
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
+                       "rows_per_step": per_step, "C": C},
+            "cpu_baseline": {"value": v, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                             "sample": f"first {per_step} rows per step, all layers in full"},
+            "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -368,7 +552,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        line = run_reference(args)
+    elif args.workload.startswith("cfg4"):
+        line = run_ours_mlp(args)
+    else:
+        line = run_ours(args)
     if line is not None:
         print(json.dumps(line), flush=True)
 
