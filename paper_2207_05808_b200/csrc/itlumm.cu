@@ -565,7 +565,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
   int CS = 0;
   size_t smem_tc = 0;
   for (int cs = 4; cs >= 1; --cs) {
-    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false).total;
+    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false, t.ST).total;
     if (smem_tc <= kSmemMax) { CS = cs; break; }
   }
   const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
@@ -599,6 +599,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
     gt.ready = P->ready; gt.consumed = P->ready + P->scratch_rows / 128;
     gt.enc_R = R; gt.enc_warps = enc_warps;
     gt.stream_b = t.stream_b ? 1 : 0;
+    gt.ST = t.ST;
     alignas(64) CUtensorMap out_map;
     memset(&out_map, 0, sizeof out_map);
     gt.tma_store = make_out_map(&out_map, gt.out, rows, P->M, ldo) ? 1 : 0;

@@ -37,7 +37,7 @@ constexpr int kTcLoaderWarp = kTcEpiWarp0 + kTcEpiWarps;       // warp 13: codes
 constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + kTcEpiWarps + 1);   // 448
 constexpr int kTcRows = 128;                                   // UMMA M
 constexpr int kKBlock = 128;                                   // bytes of K per block = 8 codebooks
-constexpr int kTcStages = 3;                                   // A ring depth (K-blocks)
+constexpr int kTcStages = 3;                                   // default A ring depth (K-blocks)
 constexpr size_t kTcBBudget = 128 * 1024;                      // resident LUT slice budget
 constexpr int kTcStage = 32 * 32 * 4;                          // epilogue staging per warp (bytes)
 constexpr size_t kSmemMax = 227 * 1024;                        // dynamic shared memory per CTA
@@ -49,6 +49,7 @@ struct TcPlan {
   int C = 0, M = 0, KB = 0, NS = 0, G = 0, tmem_cols = 0;
   int CS = 0;                    // codes ring stages (TMA path), 0 = codes path unavailable
   bool stream_b = false;         // LUT too large to stay resident: B K-blocks streamed per stage
+  int ST = kTcStages;            // ring stages (one-hot K-blocks, + LUT K-blocks when streamed)
   size_t smem = 0;
   int grid = 0;
 };
@@ -80,6 +81,7 @@ struct TcKArgs {
   // (row tile, slice) pairs u = cta + k * ncta, slice = u / ntiles (consecutive CTAs share a slice,
   // so its K-blocks stream from L2); each stage carries the one-hot K-block and the LUT K-block.
   int stream_b;
+  int ST;          // ring stages
 };
 
 // TMA tensor store of one 32x32 fp32 box (128-byte swizzled rows in shared memory) at (x=col, y=row);
@@ -145,11 +147,11 @@ struct TcSmem {
 // stream_b: no resident slice; each of the kTcStages stages holds a one-hot K-block and a LUT
 // K-block (NS x 128 B).  fused = false: no threshold/column tables.
 __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS = 0, int ldc_tma = 0,
-                                                 bool stream_b = false, bool fused = true) {
+                                                 bool stream_b = false, bool fused = true, int ST = kTcStages) {
   TcSmem s{};
   size_t o = 0;
-  s.b = o;    o += stream_b ? (size_t)kTcStages * NS * kKBlock : (size_t)KB * NS * kKBlock;
-  s.a = o;    o += (size_t)kTcStages * kTcRows * kKBlock;
+  s.b = o;    o += stream_b ? (size_t)ST * NS * kKBlock : (size_t)KB * NS * kKBlock;
+  s.a = o;    o += (size_t)ST * kTcRows * kKBlock;
   s.stg = o;  o += (size_t)kTcEpiWarps * kTcStage;
   s.codes = o; o += (size_t)CS * kTcRows * ldc_tma;
   if (!fused) C = 0;
@@ -158,7 +160,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
   s.sc = o;   o += (size_t)NS * 4;
   s.ot = o;   o += (size_t)NS * 4;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;  o += (size_t)(2 * kTcStages + 4 + 2 * CS + 1) * 8;
+  s.bar = o;  o += (size_t)(2 * ST + 4 + 2 * CS + 1) * 8;
   s.tmem = o; o += 16;
   s.total = o + 1024;                           // slack for 1024-byte alignment of the base
   return s;
@@ -173,7 +175,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
   const int CS = FUSED ? 0 : g.CS;
   static_assert(!(FUSED && SB), "the streamed-LUT mode has no fused variant");
-  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED);
+  const int ST = g.ST;                                // A (and streamed-B) ring depth
+  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED, ST);
   uint8_t* b_s = smem + L.b;
   uint8_t* codes_s = smem + L.codes;
   uint8_t* a_s = smem + L.a;
@@ -182,8 +185,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   float* sc_s = reinterpret_cast<float*>(smem + L.sc);
   float* ot_s = reinterpret_cast<float*>(smem + L.ot);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* empty_bar = full_bar + kTcStages;
-  uint64_t* accf_bar = empty_bar + kTcStages;
+  uint64_t* empty_bar = full_bar + ST;
+  uint64_t* accf_bar = empty_bar + ST;
   uint64_t* acce_bar = accf_bar + 2;
   uint64_t* codes_bar = acce_bar + 2;
   uint64_t* codes_empty = codes_bar + CS;            // producers done with a codes stage
@@ -233,7 +236,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       ot_s[i] = m < p.Mp ? __ldg(p.offtot + m) : 0.f;
     }
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kTcStages; ++s) { mbar_init(full_bar + s, kTcProducers + (SB ? 1 : 0)); mbar_init(empty_bar + s, 1); }
+      for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, kTcProducers + (SB ? 1 : 0)); mbar_init(empty_bar + s, 1); }
       for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
       for (int s = 0; s < CS; ++s) { mbar_init(codes_bar + s, 1); mbar_init(codes_empty + s, kTcProducers); }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -285,7 +288,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
             mbar_wait(empty_bar + stage, phase ^ 1);
             mbar_arrive_expect_tx(full_bar + stage, bbytes);
             bulk_g2s(b_s + (size_t)stage * bbytes, src + (size_t)kb * bbytes, bbytes, full_bar + stage);
-            if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -323,7 +326,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           }
           fence_proxy_async_smem();
           mbar_arrive(full_bar + stage);
-          if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         mbar_arrive(codes_empty + cs);                 // this producer is done with stage cs
         if (++cs == CS) { cs = 0; cph ^= 1; }
@@ -399,7 +402,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       }
       fence_proxy_async_smem();
       mbar_arrive(full_bar + stage);
-      if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      if (++stage == ST) { stage = 0; phase ^= 1; }
       if (FUSED) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -440,7 +443,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           if (kb == KB - 1) umma_commit(accf_bar + acc);
         }
         __syncwarp();
-        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+        if (++stage == ST) { stage = 0; phase ^= 1; }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -692,7 +695,13 @@ inline itlumm_status tc_set_attr(size_t smem) {
 
 inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   if (!t.ok) return ITLUMM_OK;
-  t.smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, t.stream_b, !t.stream_b).total;
+  // ring depth: 4 stages when they fit next to a 1-stage codes ring, else 3 (developer override,
+  // not ABI: ITLUMM_TC_STAGES)
+  static const int st_env = getenv("ITLUMM_TC_STAGES") ? atoi(getenv("ITLUMM_TC_STAGES")) : 0;
+  t.ST = kTcStages;
+  if (st_env >= 2 && st_env <= 6) t.ST = st_env;
+  else if (tc_smem_layout(t.C, t.KB, t.NS, 1, 16 * ((t.C + 31) / 32), t.stream_b, !t.stream_b, 4).total <= kSmemMax) t.ST = 4;
+  t.smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, t.stream_b, !t.stream_b, t.ST).total;
   if (t.smem > kSmemMax) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
   itlumm_status st;
   if ((st = tc_set_attr<true, float, false>(kSmemMax)) != ITLUMM_OK) return st;
@@ -742,6 +751,7 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
   k.pdl = pdl ? 1 : 0;
   k.stream_b = t.stream_b ? 1 : 0;
+  k.ST = t.ST;
   if (t.stream_b && fused) { g_tc_msg = "the LUT is streamed (too large to stay resident): no fused TC kernel"; return ITLUMM_EUNSUPPORTED; }
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
@@ -751,7 +761,7 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
     // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
     for (int cs = 4; cs >= 1; --cs) {
-      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused).total;
+      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused, t.ST).total;
       if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { k.CS = cs; smem = need; break; }
     }
   }
