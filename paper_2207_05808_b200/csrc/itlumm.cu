@@ -298,6 +298,10 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   itlumm_status st = configure_simt(P);
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
+  if (st == ITLUMM_OK && getenv("ITLUMM_TC_TRACE") && atoi(getenv("ITLUMM_TC_TRACE")) != 0) {
+    cudaMalloc(&P->tc.trace, (size_t)8 * 4 * kTraceEv * 8);
+    if (P->tc.trace) cudaMemset(P->tc.trace, 0, (size_t)8 * 4 * kTraceEv * 8);
+  }
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
   if (P->tc.ok) {
     P->scratch_ldc = (((C + 1) / 2) + 15) & ~15;
@@ -336,6 +340,7 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
   if (P->dmem) cudaFree(P->dmem);
   if (P->scratch) cudaFree(P->scratch);
   if (P->ready) cudaFree(P->ready);
+  if (P->tc.trace) cudaFree(P->tc.trace);
   if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
   if (P->stage) cudaFree(P->stage);
   for (auto& s : P->hs)
@@ -600,6 +605,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
     gt.enc_R = R; gt.enc_warps = enc_warps;
     gt.stream_b = t.stream_b ? 1 : 0;
     gt.ST = t.ST;
+    gt.trace = t.trace;
     alignas(64) CUtensorMap out_map;
     memset(&out_map, 0, sizeof out_map);
     gt.tma_store = make_out_map(&out_map, gt.out, rows, P->M, ldo) ? 1 : 0;
@@ -883,6 +889,16 @@ extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_
   }
   g_launches = launches;
   return ITLUMM_OK;
+}
+
+// Developer timeline (not in the ABI header): with ITLUMM_TC_TRACE=1 at plan creation every TC
+// launch of the plan records globaltimer stamps of CTAs 0..7 (producer K-block arrives, MMA tile
+// starts and K-block commits, epilogue warp-0 tile start/end, codes loads); copy them out here.
+extern "C" int itlumm_dbg_trace_copy(itlumm_plan P, uint64_t* host, int64_t n) {
+  if (!P || !P->tc.trace || !host) return 1;
+  const int64_t total = (int64_t)8 * 4 * kTraceEv;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, P->tc.trace, (size_t)std::min(n, total) * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 
 extern "C" int32_t itlumm_last_launch_count(void) { return g_launches; }

@@ -50,6 +50,7 @@ struct TcPlan {
   int CS = 0;                    // codes ring stages (TMA path), 0 = codes path unavailable
   bool stream_b = false;         // LUT too large to stay resident: B K-blocks streamed per stage
   int ST = kTcStages;            // ring stages (one-hot K-blocks, + LUT K-blocks when streamed)
+  uint64_t* trace = nullptr;     // developer timeline buffer (ITLUMM_TC_TRACE=1), 8 x 4 x kTraceEv
   size_t smem = 0;
   int grid = 0;
 };
@@ -82,7 +83,14 @@ struct TcKArgs {
   // so its K-blocks stream from L2); each stage carries the one-hot K-block and the LUT K-block.
   int stream_b;
   int ST;          // ring stages
+  uint64_t* trace; // developer timeline (ITLUMM_TC_TRACE): [8 CTAs][4 roles][kTraceEv] globaltimer stamps
 };
+constexpr int kTraceEv = 512;
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // TMA tensor store of one 32x32 fp32 box (128-byte swizzled rows in shared memory) at (x=col, y=row);
 // rows >= N and columns >= M are clipped by the tensor map bounds.
@@ -198,18 +206,53 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   const int ngroups = ncta / G;
   const int64_t ntiles = (g.N + kTcRows - 1) / kTcRows;
   // k-th work item of this CTA: (row tile, slice); false when the CTA is done
-  auto item = [&](int64_t k, int64_t& tile, int& sl) -> bool {
+  // Work balance: whole (tile, slice) items first, `full` rounds of them; the `rem` leftover items
+  // of the last round are split into `parts` column ranges (of the NC 32-column epilogue chunks)
+  // spread over the idle CTAs, so no CTA runs a whole extra tile while the others idle (the
+  // epilogue is the per-tile bottleneck; cfg2: 469 tiles on 74 CTA pairs = 6.34 rounds).
+  const int NC = NS / 32;
+  const int64_t units = SB ? ntiles * G : ntiles;       // items sharing this CTA's slice set
+  const int64_t nworkers = SB ? ncta : ngroups;
+  const int64_t worker = SB ? cta : group;
+  const int64_t full = units / nworkers, rem = units - full * nworkers;
+  int parts = 1;
+  if (rem) {
+    const int64_t pp = nworkers / rem;
+    parts = pp < 1 ? 1 : (pp > NC ? NC : (int)pp);
+  }
+  auto item4 = [&](int64_t k, int64_t& tile, int& sl, int& c0, int& c1) -> bool {
+    int64_t u;
+    c0 = 0;
+    c1 = NC;
+    if (k < full) {
+      u = worker + k * nworkers;
+    } else if (k == full && worker < rem * parts) {
+      u = full * nworkers + worker / parts;
+      const int part = (int)(worker % parts);
+      c0 = part * NC / parts;
+      c1 = (part + 1) * NC / parts;
+    } else {
+      return false;
+    }
     if (SB) {
-      const int64_t u = cta + k * ncta;
       sl = (int)(u / ntiles);
       tile = u - (int64_t)sl * ntiles;
-      return u < ntiles * G;
+    } else {
+      sl = slice;
+      tile = u;
     }
-    sl = slice;
-    tile = group + k * ngroups;
-    return tile < ntiles;
+    return true;
+  };
+  auto item = [&](int64_t k, int64_t& tile, int& sl) -> bool {
+    int c0, c1;
+    return item4(k, tile, sl, c0, c1);
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* trace = (g.trace && cta < 8) ? g.trace + (size_t)cta * 4 * kTraceEv : nullptr;
+  int tev[4] = {0, 0, 0, 0};
+  auto stamp = [&](int role) {                          // role: 0 producer, 1 MMA, 2 epilogue, 3 loader
+    if (trace && tev[role] < kTraceEv) trace[role * kTraceEv + tev[role]++] = gtimer();
+  };
 
   // ---- prologue: the resident LUT slice (already swizzled in HBM) by bulk copy (TMA engine),
   // thresholds, columns, scales by the threads; only the MMA warp waits for the slice.
@@ -272,7 +315,13 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           const uint32_t need = (uint32_t)((rows + g.enc_R - 1) / g.enc_R);
           spin_until_geq(g.ready + tile, need);
           asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
-          if (atomicAdd(g.consumed + tile, 1u) == (uint32_t)G - 1) {   // last slice to look
+          // items reading this tile: one per slice, `parts` for leftover (split) units
+          uint32_t nread = 0;
+          for (int s2 = 0; s2 < G; ++s2) {
+            const int64_t u2 = SB ? (int64_t)s2 * ntiles + tile : tile;
+            nread += (u2 >= full * nworkers) ? (uint32_t)parts : 1u;
+          }
+          if (atomicAdd(g.consumed + tile, 1u) == nread - 1) {   // last reader to look
             g.ready[tile] = 0u;
             g.consumed[tile] = 0u;
           }
@@ -280,6 +329,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         const uint32_t bytes = (uint32_t)(rows * g.ldc);
         mbar_arrive_expect_tx(codes_bar + cs, bytes);
         bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
+        stamp(3);
         if (++cs == CS) { cs = 0; cph ^= 1; }
         if (SB) {                                     // this item's LUT K-blocks, one per stage
           const uint32_t bbytes = (uint32_t)NS * kKBlock;
@@ -326,6 +376,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           }
           fence_proxy_async_smem();
           mbar_arrive(full_bar + stage);
+          if (r == 0) stamp(0);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         mbar_arrive(codes_empty + cs);                 // this producer is done with stage cs
@@ -364,14 +415,17 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         }
       }
     };
-    int64_t tile = group;
-    int kb = 0;
-    if (tile < ntiles) load(tile, 0, vc, cc);
-    while (tile < ntiles) {
-      int64_t ntile = tile;
+    // the same item sequence as the MMA and epilogue warps (including split leftover items)
+    int64_t k = 0, tile = 0;
+    int sl = 0, kb = 0;
+    bool more = item(0, tile, sl);
+    if (more) load(tile, 0, vc, cc);
+    while (more) {
+      int64_t ntile = tile, nk = k;
       int nkb = kb + 1;
-      if (nkb == KB) { nkb = 0; ntile += ngroups; }
-      if (ntile < ntiles) load(ntile, nkb, vn, cn);
+      bool nmore = true;
+      if (nkb == KB) { nkb = 0; ++nk; nmore = item(nk, ntile, sl); }
+      if (nmore) load(ntile, nkb, vn, cn);
       const bool valid = tile * kTcRows + r < g.N;
       uint32_t code[8];
 #pragma unroll
@@ -413,6 +467,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       }
       tile = ntile;
       kb = nkb;
+      k = nk;
+      more = nmore;
     }
     }
   } else if (warp == kTcMmaWarp) {
@@ -427,6 +483,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     int sl;
     for (int64_t k = 0; item(k, tile, sl); ++k) {
       mbar_wait(acce_bar + acc, acc_phase ^ 1);      // epilogue drained this accumulator
+      if (lane == 0) stamp(1);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(acc * NS);
       for (int kb = 0; kb < KB; ++kb) {
@@ -440,6 +497,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
             umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
                     (kb | ks) != 0);
           umma_commit(empty_bar + stage);             // frees the A stage when these MMAs finish
+          stamp(1);
           if (kb == KB - 1) umma_commit(accf_bar + acc);
         }
         __syncwarp();
@@ -467,16 +525,17 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       uint32_t acc_phase = 0;
       bool pending = false;
       int64_t tile;
-      int sl;
-      for (int64_t k = 0; item(k, tile, sl); ++k) {
+      int sl, c0, c1;
+      for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
         mbar_wait(accf_bar + acc, acc_phase);
         tc_fence_after();
+        if (warp == kTcEpiWarp0 && lane == 0) stamp(2);
         const int m0 = sl * NS;
         const float* scp = SB ? p.scale + m0 : sc_s;   // scale/offtot of this slice's columns
         const float* otp = SB ? p.offtot + m0 : ot_s;
         const int row0 = (int)(tile * kTcRows) + q * 32;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
-        for (int j0 = h * 32; j0 < NS; j0 += 64) {
+        for (int j0 = (c0 + ((h - c0) & 1)) * 32; j0 < c1 * 32; j0 += 64) {
           uint32_t v[32];
           tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
           tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -515,6 +574,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         }
         tc_fence_before();
         mbar_arrive(acce_bar + acc);
+        if (warp == kTcEpiWarp0 && lane == 0) stamp(2);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (lane == 0) bulk_wait0();
@@ -527,8 +587,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     int acc = 0;
     uint32_t acc_phase = 0;
     int64_t tile;
-    int sl;
-    for (int64_t k = 0; item(k, tile, sl); ++k) {
+    int sl, c0, c1;
+    for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
       mbar_wait(accf_bar + acc, acc_phase);
       tc_fence_after();
       const int m0 = sl * NS;
@@ -549,6 +609,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       for (int i = 0; i < kMaxChunks; ++i) {
         const int j0 = h * 32 + i * 64;
         if (j0 >= NS) break;
+        if (j0 < c0 * 32 || j0 >= c1 * 32) continue;   // outside this item's column range
         uint32_t v[32];
         tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
         tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -752,6 +813,7 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.pdl = pdl ? 1 : 0;
   k.stream_b = t.stream_b ? 1 : 0;
   k.ST = t.ST;
+  k.trace = t.trace;
   if (t.stream_b && fused) { g_tc_msg = "the LUT is streamed (too large to stay resident): no fused TC kernel"; return ITLUMM_EUNSUPPORTED; }
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);

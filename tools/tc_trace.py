@@ -1,0 +1,57 @@
+#!/usr/bin/env python
+"""Developer timeline of the TC kernel (ITLUMM_TC_TRACE=1): per-role event stamps of CTAs 0..7 of
+the last launch.  Prints per-tile MMA start / epilogue start-end and K-block cadence (ns)."""
+import ctypes
+import json
+import os
+import sys
+
+os.environ["ITLUMM_TC_TRACE"] = "1"
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2207_05808_b200 import Plan, fit_layer, _lib  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+mode = sys.argv[2] if len(sys.argv) > 2 else "acc"      # acc: lut_accumulate; sp: fused TC_SP amm
+cfg = synth.CONFIGS[name]
+w = synth.workload(name, n_rows=cfg["N"])
+bf16 = cfg["dtype"] == "bf16"
+p = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
+plan = Plan(p, algo="tc" if mode == "acc" else "tc_sp")
+A = torch.from_numpy(w["A"].view(np.int16) if bf16 else w["A"]).cuda()
+if bf16:
+    A = A.view(torch.bfloat16)
+codes = plan.encode(A)
+out = torch.empty((cfg["N"], cfg["M"]), device="cuda")
+for _ in range(5):
+    if mode == "acc":
+        plan.lut_accumulate(codes, out=out, relu=cfg["relu"])
+    else:
+        plan.amm(A, out=out, relu=cfg["relu"])
+torch.cuda.synchronize()
+lib = _lib.load()
+lib.itlumm_dbg_trace_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+KE = 512
+buf = np.zeros(8 * 4 * KE, np.uint64)
+assert lib.itlumm_dbg_trace_copy(plan._h, buf.ctypes.data_as(ctypes.c_void_p), buf.size) == 0
+t = buf.reshape(8, 4, KE).astype(np.int64)
+t0 = t[t > 0].min()
+res = {}
+for cta in range(4):
+    ev = {}
+    for role, nm in enumerate(["producer_kb", "mma", "epi", "loader"]):
+        x = t[cta, role]
+        x = x[x > 0] - t0
+        ev[nm] = x.tolist()
+    res[cta] = ev
+    pk, mm, ep, ld = (np.array(ev[k]) for k in ("producer_kb", "mma", "epi", "loader"))
+    print(f"CTA {cta}: producer K-blocks {len(pk)}, mma events {len(mm)}, epi events {len(ep)}, loads {len(ld)}")
+    print("  loader   ", ld[:10].tolist())
+    print("  producer ", pk[:24].tolist())
+    print("  mma      ", mm[:30].tolist())
+    print("  epi s/e  ", ep.tolist())
+    print("  end      ", max(pk.max(initial=0), mm.max(initial=0), ep.max(initial=0)))
+json.dump(res, open(os.path.join("gpurun_out", f"tc_trace_{name}_{mode}.json"), "w"))
