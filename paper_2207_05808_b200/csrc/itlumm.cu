@@ -299,8 +299,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
   if (st == ITLUMM_OK && getenv("ITLUMM_TC_TRACE") && atoi(getenv("ITLUMM_TC_TRACE")) != 0) {
-    cudaMalloc(&P->tc.trace, (size_t)8 * 4 * kTraceEv * 8);
-    if (P->tc.trace) cudaMemset(P->tc.trace, 0, (size_t)8 * 4 * kTraceEv * 8);
+    cudaMalloc(&P->tc.trace, (size_t)16 * 4 * kTraceEv * 8);
+    if (P->tc.trace) cudaMemset(P->tc.trace, 0, (size_t)16 * 4 * kTraceEv * 8);
   }
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
   if (P->tc.ok) {
@@ -392,7 +392,8 @@ static itlumm_status check_A(itlumm_plan P, const void* A, itlumm_dtype dtype, i
 
 // Rows per stage R and ring depth S of the streaming encoder for rows of rb bytes, or false if
 // the rows cannot be bulk-copied.  pow2: R a power of two dividing 128 (TC_SP ready counters).
-static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2, int* Rout, int* Sout) {
+static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2, int* Rout, int* Sout,
+                       int inflight_override_kb = 0, int max_stages = 8) {
   // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
   // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
   // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
@@ -410,7 +411,8 @@ static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2,
     while (r2 * 2 <= R && r2 * 2 <= 128) r2 *= 2;
     R = r2;
   }
-  int S = (int)std::max<int64_t>(2, std::min<int64_t>(8, ((int64_t)inflight_kb * 1024 + R * rb / 2) / (R * rb)));
+  const int64_t infl = inflight_override_kb > 0 ? inflight_override_kb : inflight_kb;
+  int S = (int)std::max<int64_t>(2, std::min<int64_t>(max_stages, (infl * 1024 + R * rb / 2) / (R * rb)));
   while (S >= 2 && enc_smem_bytes(P->C, R, S, (int)rb) > 200 * 1024) --S;
   if (S < 2) return false;
   *Rout = R;
@@ -563,18 +565,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
   const int64_t rb = (int64_t)P->D * es;
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
   const int enc_warps = kTcThreads / 32 - 1;
-  int R = 0, S = 0;
-  if (!P->coop || !aligned || !enc_tiling(P, rb, enc_warps, true, &R, &S))
-    return fail(ITLUMM_EUNSUPPORTED, "TC_SP needs cooperative launch and 16-byte aligned rows");
   const TcPlan& t = P->tc;
-  int CS = 0;
-  size_t smem_tc = 0;
-  for (int cs = 4; cs >= 1; --cs) {
-    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false, t.ST).total;
-    if (smem_tc <= kSmemMax) { CS = cs; break; }
-  }
-  const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
-  if (CS == 0 || smem > kSmemMax) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: shared memory budget exceeded");
   // split: encoder share ~ bytes read / (bytes read + 1.25 x bytes written) (developer override:
   // ITLUMM_SP_ENC_CTAS)
   static const int enc_override = getenv("ITLUMM_SP_ENC_CTAS") ? atoi(getenv("ITLUMM_SP_ENC_CTAS")) : 0;
@@ -584,6 +575,21 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
   if (T < t.G) T = t.G;
   E = P->num_sms - T;
   if (E < 1) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: too few SMs for the split");
+  // fewer encoder SMs each keep proportionally more bytes in flight (same total as the
+  // standalone encoder), with up to 16 stages (the TC role's shared memory is there anyway)
+  static const int sp_infl = getenv("ITLUMM_SP_INFLIGHT_KB") ? atoi(getenv("ITLUMM_SP_INFLIGHT_KB")) : 0;
+  const int infl_kb = sp_infl > 0 ? sp_infl : (int)std::min<int64_t>(190, 100LL * P->num_sms / E);
+  int R = 0, S = 0;
+  if (!P->coop || !aligned || !enc_tiling(P, rb, enc_warps, true, &R, &S, infl_kb, 16))
+    return fail(ITLUMM_EUNSUPPORTED, "TC_SP needs cooperative launch and 16-byte aligned rows");
+  int CS = 0;
+  size_t smem_tc = 0;
+  for (int cs = 4; cs >= 1; --cs) {
+    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false, t.ST).total;
+    if (smem_tc <= kSmemMax) { CS = cs; break; }
+  }
+  const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
+  if (CS == 0 || smem > kSmemMax) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: shared memory budget exceeded");
   std::lock_guard<std::mutex> lk(P->scratch_mu);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CUDA_TRY(cudaStreamIsCapturing(s, &cap));
@@ -896,7 +902,7 @@ extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_
 // starts and K-block commits, epilogue warp-0 tile start/end, codes loads); copy them out here.
 extern "C" int itlumm_dbg_trace_copy(itlumm_plan P, uint64_t* host, int64_t n) {
   if (!P || !P->tc.trace || !host) return 1;
-  const int64_t total = (int64_t)8 * 4 * kTraceEv;
+  const int64_t total = (int64_t)16 * 4 * kTraceEv;
   cudaDeviceSynchronize();
   return cudaMemcpy(host, P->tc.trace, (size_t)std::min(n, total) * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }

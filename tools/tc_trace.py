@@ -35,9 +35,9 @@ torch.cuda.synchronize()
 lib = _lib.load()
 lib.itlumm_dbg_trace_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
 KE = 512
-buf = np.zeros(8 * 4 * KE, np.uint64)
+buf = np.zeros(16 * 4 * KE, np.uint64)
 assert lib.itlumm_dbg_trace_copy(plan._h, buf.ctypes.data_as(ctypes.c_void_p), buf.size) == 0
-t = buf.reshape(8, 4, KE).astype(np.int64)
+t = buf.reshape(16, 4, KE).astype(np.int64)
 t0 = t[t > 0].min()
 res = {}
 for cta in range(4):
@@ -54,4 +54,10 @@ for cta in range(4):
     print("  mma      ", mm[:30].tolist())
     print("  epi s/e  ", ep.tolist())
     print("  end      ", max(pk.max(initial=0), mm.max(initial=0), ep.max(initial=0)))
+for cta in range(8, 10):
+    pi, cd, pu = (t[cta, r][t[cta, r] > 0] - t0 for r in range(3))
+    print(f"encoder CTA {cta - 8}: issues {len(pi)}, consumed {len(cd)}, published {len(pu)}")
+    print("  issue    ", pi[:24].tolist())
+    print("  consumed ", cd[:24].tolist())
+    print("  publish  ", pu[:24].tolist())
 json.dump(res, open(os.path.join("gpurun_out", f"tc_trace_{name}_{mode}.json"), "w"))
