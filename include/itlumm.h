@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define ITLUMM_ABI_VERSION 2
+#define ITLUMM_ABI_VERSION 3
 
 typedef enum {
   ITLUMM_OK = 0,
@@ -72,6 +72,16 @@ typedef enum {
   ITLUMM_ALGO_TC_SP = 4
 } itlumm_algo;
 
+/* Summation over codebooks (a3).
+ *   EXACT : acc[m] = sum_c lut[c][code_c][m], exact in int32 (reading R7; the default).
+ *   AVG16 : MADDNESS's "fast rounded 8-bit summation" (reading R22): codebooks in
+ *           groups of 16 (C % 16 == 0), per output a 4-level tree of per-byte rounding averages
+ *           avg(a,b) = (a+b+1)>>1 over the group's 16 entries (pairs (0,1),(2,3),... per level),
+ *           acc[m] = sum of the group results; y = fmaf(16*scale, (float)acc, offavg) with
+ *           offavg = (float)((double)C*offset + bias - 16*(C/16)*(double)scale) (the tree's +1
+ *           expected bias per group removed).  CUDA-core kernels only. */
+typedef enum { ITLUMM_SUM_EXACT = 0, ITLUMM_SUM_AVG16 = 1 } itlumm_summation;
+
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */
 
 /* Fitted layer parameters.  HOST pointers, read only during itlumm_plan_create (copied). */
@@ -104,6 +114,11 @@ itlumm_status itlumm_plan_destroy(itlumm_plan plan);
 
 /* Select the kernel family (default AUTO).  Not thread-safe against concurrent launches. */
 itlumm_status itlumm_plan_set_algo(itlumm_plan plan, itlumm_algo algo);
+
+/* Select the summation (default EXACT).  AVG16 needs C % 16 == 0 (else EINVAL) and runs on the
+ * CUDA-core kernels whatever the algo (acc outputs are then the group-average sums).  Not
+ * thread-safe against concurrent launches. */
+itlumm_status itlumm_plan_set_summation(itlumm_plan plan, itlumm_summation summation);
 
 /* Query plan dims: any out-pointer may be NULL.  lut_bytes = 16*C*M. */
 itlumm_status itlumm_plan_info(itlumm_plan plan, int32_t* D, int32_t* C, int32_t* M,

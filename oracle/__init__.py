@@ -51,6 +51,8 @@ def _load():
                                        P, ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P, P, P,
                                        ctypes.c_int, P, P, P, ctypes.c_int]
             lib.oracle_amm.restype = ctypes.c_int
+            lib.oracle_amm2.argtypes = lib.oracle_amm.argtypes + [ctypes.c_int]
+            lib.oracle_amm2.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -60,8 +62,9 @@ def _ptr(a):
 
 
 def amm(params: dict, A: np.ndarray, relu: bool, dtype: str = "f32", want_codes: bool = False,
-        want_acc: bool = False, want_y: bool = True, nthreads: int = 1):
+        want_acc: bool = False, want_y: bool = True, nthreads: int = 1, summation: str = "exact"):
     """Run the oracle inference on rows A (N x lda; fp32, or uint16 bf16 bits when dtype='bf16').
+    summation: "exact" (reading R7) or "avg16" (MADDNESS rounded averaging tree, reading R22).
 
     Returns dict(codes=[N][C] uint8 or None, acc=[N][M] int64 or None, y=[N][M] fp32 or None)."""
     lib = _load()
@@ -87,9 +90,10 @@ def amm(params: dict, A: np.ndarray, relu: bool, dtype: str = "f32", want_codes:
     codes = np.zeros((N, C), dtype=np.uint8) if want_codes else None
     acc = np.zeros((N, M), dtype=np.int64) if want_acc else None
     y = np.zeros((N, M), dtype=np.float32) if want_y else None
-    st = lib.oracle_amm(N, D, C, M, _ptr(A), dt, lda, _ptr(perm), _ptr(bnd), _ptr(sd), _ptr(thr),
-                        _ptr(lut), _ptr(scale), _ptr(off), _ptr(bias), int(bool(relu)),
-                        _ptr(codes), _ptr(acc), _ptr(y), int(nthreads))
+    st = lib.oracle_amm2(N, D, C, M, _ptr(A), dt, lda, _ptr(perm), _ptr(bnd), _ptr(sd), _ptr(thr),
+                         _ptr(lut), _ptr(scale), _ptr(off), _ptr(bias), int(bool(relu)),
+                         _ptr(codes), _ptr(acc), _ptr(y), int(nthreads),
+                         {"exact": 0, "avg16": 1}[summation])
     if st != 0:
         raise RuntimeError(f"oracle_amm failed with status {st}")
     return dict(codes=codes, acc=acc, y=y)

@@ -83,6 +83,11 @@ class Plan:
         _lib.check(self._lib.itlumm_plan_set_algo(self._h, _lib.ALGO[algo]))
         self.algo = algo
 
+    def set_summation(self, summation: str):
+        """"exact" (default) or "avg16" (MADDNESS rounded averaging tree; C % 16 == 0)."""
+        _lib.check(self._lib.itlumm_plan_set_summation(self._h, _lib.SUMMATION[summation]))
+        self.summation = summation
+
     @property
     def last_launch_count(self) -> int:
         return int(self._lib.itlumm_last_launch_count())

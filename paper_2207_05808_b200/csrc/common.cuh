@@ -19,6 +19,7 @@ struct DevPlan {
   const uint8_t* lut;     // [C][16][Mp] uint8 LUT, Mp = roundup(M,16), zero padded
   const float* scale;     // [Mp]
   const float* offtot;    // [Mp] (float)((double)C*lo + bias)
+  const float* offavg;    // [Mp] avg16 summation: (float)((double)C*lo + bias - 16*(C/16)*(double)scale)
   int D, C, M, Mp;
 };
 

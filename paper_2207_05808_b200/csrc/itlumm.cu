@@ -55,6 +55,7 @@ struct itlumm_plan_s {
   int D = 0, C = 0, M = 0, Mp = 0;
   int num_sms = 0;
   itlumm_algo algo = ITLUMM_ALGO_AUTO;
+  itlumm_summation summation = ITLUMM_SUM_EXACT;
   void* dmem = nullptr;  // one allocation holding every device parameter
   DevPlan dp{};
   SimtCfg simt{};
@@ -83,14 +84,14 @@ static bool finite_all(const float* v, int n) {
 
 typedef void (*lut_kernel_t)(DevPlan, LutArgs);
 
-template <bool FUSED, typename T>
+template <bool FUSED, typename T, bool AVG = false>
 static lut_kernel_t pick_lut_kernel(int MS) {
   switch (MS) {
-    case 16: return k_lut<16, FUSED, T>;
-    case 32: return k_lut<32, FUSED, T>;
-    case 64: return k_lut<64, FUSED, T>;
-    case 128: return k_lut<128, FUSED, T>;
-    case 256: return k_lut<256, FUSED, T>;
+    case 16: return k_lut<16, FUSED, T, AVG>;
+    case 32: return k_lut<32, FUSED, T, AVG>;
+    case 64: return k_lut<64, FUSED, T, AVG>;
+    case 128: return k_lut<128, FUSED, T, AVG>;
+    case 256: return k_lut<256, FUSED, T, AVG>;
   }
   return nullptr;
 }
@@ -133,6 +134,9 @@ static itlumm_status configure_simt(itlumm_plan_s* P) {
       if ((st = set_smem(kf32, s.smem_fused)) != ITLUMM_OK) return st;
       if ((st = set_smem(kbf, s.smem_fused)) != ITLUMM_OK) return st;
       if ((st = set_smem(kc, s.smem_codes)) != ITLUMM_OK) return st;
+      if ((st = set_smem(pick_lut_kernel<true, float, true>(MS), s.smem_fused)) != ITLUMM_OK) return st;
+      if ((st = set_smem(pick_lut_kernel<true, uint16_t, true>(MS), s.smem_fused)) != ITLUMM_OK) return st;
+      if ((st = set_smem(pick_lut_kernel<false, float, true>(MS), s.smem_codes)) != ITLUMM_OK) return st;
       int occ_f = 0, occ_c = 0;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf32, kLutThreads, s.smem_fused));
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, kLutThreads, s.smem_codes));
@@ -248,17 +252,21 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   std::vector<uint8_t> qt;
   tc_layout_host(C, M, p->lut, &P->tc, qt);
   const int Mpad = std::max(Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0);   // slice columns past M read 0
-  std::vector<float> scale(Mpad, 0.f), offtot(Mpad, 0.f);
+  std::vector<float> scale(Mpad, 0.f), offtot(Mpad, 0.f), offavg(Mpad, 0.f);
   for (int m = 0; m < M; ++m) {
     scale[m] = p->scale[m];
     const double b = p->bias ? (double)p->bias[m] : 0.0;
     offtot[m] = (float)((double)C * (double)p->offset[m] + b);   // reading R8
+    // avg16 summation (reading R22): the rounding-average tree over-estimates each group mean by
+    // +1 in expectation; 16 * (C/16) * scale removes it
+    offavg[m] = (float)((double)C * (double)p->offset[m] + b - 16.0 * (C / 16) * (double)p->scale[m]);
   }
 
   // one device allocation
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t o_cols = 0, o_thr = o_cols + al(cols.size() * 4), o_lut = o_thr + al(thr_t.size() * 4),
-               o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mpad * 4), o_qt = o_ot + al((size_t)Mpad * 4),
+               o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mpad * 4), o_oa = o_ot + al((size_t)Mpad * 4),
+               o_qt = o_oa + al((size_t)Mpad * 4),
                total = o_qt + al(qt.size());
   int prev = 0;
   cudaGetDevice(&prev);
@@ -280,7 +288,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   struct { size_t off; const void* src; size_t n; } cp[] = {
       {o_cols, cols.data(), cols.size() * 4}, {o_thr, thr_t.data(), thr_t.size() * 4},
       {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mpad * 4},
-      {o_ot, offtot.data(), (size_t)Mpad * 4},  {o_qt, qt.data(), qt.size()}};
+      {o_ot, offtot.data(), (size_t)Mpad * 4},  {o_oa, offavg.data(), (size_t)Mpad * 4},
+      {o_qt, qt.data(), qt.size()}};
   for (auto& c : cp) {
     if (!c.n) continue;
     e = cudaMemcpy(base + c.off, c.src, c.n, cudaMemcpyHostToDevice);
@@ -291,6 +300,7 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   P->dp.lut = base + o_lut;
   P->dp.scale = (const float*)(base + o_sc);
   P->dp.offtot = (const float*)(base + o_ot);
+  P->dp.offavg = (const float*)(base + o_oa);
   P->dp.D = P->D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
   P->tc.qt = qt.empty() ? nullptr : base + o_qt;
   cudaFuncSetAttribute((const void*)k_encode_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -358,6 +368,16 @@ extern "C" itlumm_status itlumm_plan_set_algo(itlumm_plan P, itlumm_algo algo) {
       algo != ITLUMM_ALGO_TC_SP)
     return fail(ITLUMM_EINVAL, "bad algo %d", (int)algo);
   P->algo = algo;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_set_summation(itlumm_plan P, itlumm_summation s) {
+  g_err.clear();
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (s != ITLUMM_SUM_EXACT && s != ITLUMM_SUM_AVG16) return fail(ITLUMM_EINVAL, "bad summation %d", (int)s);
+  if (s == ITLUMM_SUM_AVG16 && P->C % 16 != 0)
+    return fail(ITLUMM_EINVAL, "avg16 summation needs C %% 16 == 0 (C = %d)", P->C);
+  P->summation = s;
   return ITLUMM_OK;
 }
 
@@ -472,7 +492,7 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
 }
 
 static bool use_tc(itlumm_plan P) {
-  if (P->algo == ITLUMM_ALGO_SIMT) return false;
+  if (P->algo == ITLUMM_ALGO_SIMT || P->summation != ITLUMM_SUM_EXACT) return false;
   if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
   return tc_preferred(P->tc, P->simt.MS != 0);
 }
@@ -481,7 +501,7 @@ static bool use_tc(itlumm_plan P) {
 // the tensor-core tiling splits M over several CTAs (a fused kernel would repeat the gather
 // and the tree walks once per M slice).
 static bool use_pipe(itlumm_plan P) {
-  if (!P->tc.ok) return false;
+  if (!P->tc.ok || P->summation != ITLUMM_SUM_EXACT) return false;
   if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
   // a streamed LUT has no fused TC kernel: AUTO pipes it through the encoder
   return P->algo == ITLUMM_ALGO_AUTO && (P->tc.G > 1 || P->tc.stream_b);
@@ -514,9 +534,15 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
   int grid = fused ? c.grid_fused : c.grid_codes;
   const int64_t maxgrid = (int64_t)c.G * ntiles;
   if (grid > maxgrid) grid = (int)maxgrid;
-  lut_kernel_t k = fused ? (dtype == ITLUMM_BF16 ? pick_lut_kernel<true, uint16_t>(c.MS)
-                                                 : pick_lut_kernel<true, float>(c.MS))
-                         : pick_lut_kernel<false, float>(c.MS);
+  lut_kernel_t k;
+  if (P->summation == ITLUMM_SUM_AVG16)
+    k = fused ? (dtype == ITLUMM_BF16 ? pick_lut_kernel<true, uint16_t, true>(c.MS)
+                                     : pick_lut_kernel<true, float, true>(c.MS))
+              : pick_lut_kernel<false, float, true>(c.MS);
+  else
+    k = fused ? (dtype == ITLUMM_BF16 ? pick_lut_kernel<true, uint16_t>(c.MS)
+                                      : pick_lut_kernel<true, float>(c.MS))
+              : pick_lut_kernel<false, float>(c.MS);
   k<<<grid, kLutThreads, fused ? c.smem_fused : c.smem_codes, s>>>(P->dp, g);
   CUDA_TRY(cudaGetLastError());
   g_launches = 1;

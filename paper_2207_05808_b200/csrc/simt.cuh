@@ -80,7 +80,10 @@ __host__ __device__ inline size_t lut_smem_bytes(int C, int MS, int R, int S, bo
   return b;
 }
 
-template <int MS, bool FUSED, typename T>
+// AVG: MADDNESS-style rounded 8-bit summation (reading R22): per group of 16 codebooks a
+// 4-level tree of per-byte rounding averages (__vavgu4 on the lane's 16 LUT bytes), group results
+// summed exactly; dequant with 16*scale and the bias-corrected offset (DevPlan.offavg).  C % 16 == 0.
+template <int MS, bool FUSED, typename T, bool AVG = false>
 __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
   constexpr int LPR = MS / 16;               // consumer lanes per row (16 columns each)
   constexpr int RPP = kConsumers / LPR;      // rows per consumer pass
@@ -218,8 +221,8 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int m = mbase + j;
-      sc[j] = (m < p.Mp) ? __ldg(p.scale + m) : 0.f;
-      ot[j] = (m < p.Mp) ? __ldg(p.offtot + m) : 0.f;
+      sc[j] = (m < p.Mp) ? (AVG ? 16.0f : 1.0f) * __ldg(p.scale + m) : 0.f;   // x16 is exact
+      ot[j] = (m < p.Mp) ? __ldg((AVG ? p.offavg : p.offtot) + m) : 0.f;
     }
     const uint32_t one = g.one;
     const bool full = g.vec_out && (mbase + 16 <= p.M);
@@ -235,6 +238,33 @@ __global__ void __launch_bounds__(kLutThreads, 1) k_lut(DevPlan p, LutArgs g) {
         for (int j = 0; j < 16; ++j) acc[j] = 0;
         const uint32_t* offs = ring + ((size_t)s * R + rl) * C4;
         const uint8_t* lbase = lut_s + lane * 16;
+        if (AVG) {
+          for (int g0 = 0; g0 < C4; g0 += 16) {
+            uint4 w[16];
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const uint4 o = *reinterpret_cast<const uint4*>(offs + g0 + i);
+              w[i + 0] = *reinterpret_cast<const uint4*>(lbase + o.x);
+              w[i + 1] = *reinterpret_cast<const uint4*>(lbase + o.y);
+              w[i + 2] = *reinterpret_cast<const uint4*>(lbase + o.z);
+              w[i + 3] = *reinterpret_cast<const uint4*>(lbase + o.w);
+            }
+#pragma unroll
+            for (int n = 16; n > 1; n >>= 1)
+#pragma unroll
+              for (int i = 0; i < n / 2; ++i) {
+                w[i].x = __vavgu4(w[2 * i].x, w[2 * i + 1].x);
+                w[i].y = __vavgu4(w[2 * i].y, w[2 * i + 1].y);
+                w[i].z = __vavgu4(w[2 * i].z, w[2 * i + 1].z);
+                w[i].w = __vavgu4(w[2 * i].w, w[2 * i + 1].w);
+              }
+            const uint32_t ww[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[4 * i + b] += (ww[i] >> (8 * b)) & 0xFFu;
+          }
+        } else
         for (int cb = 0; cb < C4; cb += 256) {      // 16-bit lanes are exact for <= 257 adds
           uint32_t ev[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
           const int ce = min(C4, cb + 256);

@@ -29,7 +29,7 @@ def test_exports_every_header_symbol(lib):
     assert set(syms) == set(_lib.EXPORTS), syms
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.itlumm_abi_version() == 2
+    assert lib.itlumm_abi_version() == 3
 
 
 def test_sm100a_only_binary():
@@ -86,6 +86,7 @@ def test_calls_reject_null_plan(lib):
     assert lib.itlumm_lut_accumulate(None, None, 1, 1, None, 3, None, 3, 0, None) == _lib.EINVAL
     assert lib.itlumm_amm_host(None, None, 0, 8, 1, None, 3, 0, None) == _lib.EINVAL
     assert lib.itlumm_plan_set_algo(None, 0) == _lib.EINVAL
+    assert lib.itlumm_plan_set_summation(None, 1) == _lib.EINVAL
     assert lib.itlumm_plan_destroy(None) == _lib.OK
     assert lib.itlumm_mlp_forward(None, None, 0, 8, 1, None, 3, None) == _lib.EINVAL
     assert lib.itlumm_mlp_info(None, None, None) == _lib.EINVAL

@@ -379,3 +379,65 @@ def test_fit_lut_size_and_code_range_invariants():
     Tsum = sum(p["T"][c][codes[:, c]] for c in range(8))
     deq = acc * p["scale64"] + 8 * p["lo64"]
     assert np.all(np.abs(deq - Tsum) <= 8 * p["scale64"] / 2 * (1 + 1e-9))
+
+
+# ---------------------------------------------------------------------------- f3: avg16 summation
+def _avg_params(C, M, lut, scale=None, offset=None, bias=None):
+    """Identity-dim trees (one input dim per codebook, thresholds split [0,16) into codes)."""
+    thr = np.tile(bst_thresholds(np.arange(1, 16) - 0.5), (C, 1))
+    return params_from(C, C, M, np.zeros((C, 4), np.int32), thr, lut, scale=scale, offset=offset, bias=bias)
+
+
+def test_avg16_golden_tree_examples():
+    """tests/golden/avg16_tree_examples.txt: hand-derived 4-level rounding-average trees."""
+    for name, vals, want in read_golden("avg16_tree_examples.txt"):
+        v = np.array([int(x) for x in vals.split()], np.int64)
+        lut = np.zeros((16, 16, 1), np.uint8)
+        lut[:, :, 0] = v[:, None]                      # every code of codebook c looks up v[c]
+        p = _avg_params(16, 1, lut)
+        out = oracle.amm(p, np.zeros((1, 16), np.float32), relu=False, want_acc=True, summation="avg16")
+        assert int(out["acc"][0, 0]) == int(want), name
+
+
+def test_avg16_multiples_of_16_are_exact_and_bias_bounds():
+    """Entries that are multiples of 16 never round: acc_avg * 16 == acc_exact.  For any entries
+    each group's tree result exceeds the group mean by d with 0 <= d < 2, and E[d] = 1 (the
+    per-level rounding adds 1/4 in expectation at each of the 4 levels, halved upwards: 4 x 1/4)."""
+    rng = np.random.default_rng(7)
+    C, M, N = 64, 40, 3000
+    A = rng.uniform(0, 16, size=(N, C)).astype(np.float32)
+    lut16 = (rng.integers(0, 16, size=(C, 16, M)) * 16).astype(np.uint8)
+    p = _avg_params(C, M, lut16)
+    ex = oracle.amm(p, A, relu=False, want_acc=True)["acc"]
+    av = oracle.amm(p, A, relu=False, want_acc=True, summation="avg16")["acc"]
+    assert np.array_equal(av * 16, ex)
+    lut = rng.integers(0, 256, size=(C, 16, M)).astype(np.uint8)
+    p = _avg_params(C, M, lut)
+    ex = oracle.amm(p, A, relu=False, want_acc=True)["acc"].astype(np.float64)
+    av = oracle.amm(p, A, relu=False, want_acc=True, summation="avg16")["acc"].astype(np.float64)
+    G = C // 16
+    d = av - ex / 16.0
+    assert d.min() >= 0 and d.max() < 2 * G
+    assert abs(d.mean() / G - 1.0) < 0.01, d.mean() / G
+
+
+def test_avg16_dequant_is_one_rounding_and_rejects_ragged_C():
+    """y = fmaf(16*scale, acc, offavg) with offavg = (float)(C*lo + bias - 16*(C/16)*scale): the
+    exact rational 16*scale*acc + offavg rounded once to fp32 (reading R22); C % 16 != 0 refused."""
+    rng = np.random.default_rng(8)
+    C, M = 32, 7
+    lut = rng.integers(0, 256, size=(C, 16, M)).astype(np.uint8)
+    scale = rng.uniform(1e-3, 1e-2, M).astype(np.float32)
+    off = rng.normal(0, 0.1, M).astype(np.float32)
+    bias = rng.normal(0, 0.1, M).astype(np.float32)
+    p = _avg_params(C, M, lut, scale=scale, offset=off, bias=bias)
+    A = rng.uniform(0, 16, size=(50, C)).astype(np.float32)
+    out = oracle.amm(p, A, relu=False, want_acc=True, summation="avg16")
+    for m in range(M):
+        offavg = np.float32(float(C) * float(off[m]) + float(bias[m]) - 16.0 * (C // 16) * float(scale[m]))
+        for n in range(50):
+            exact = Fraction(float(np.float32(16 * scale[m]))) * int(out["acc"][n, m]) + Fraction(float(offavg))
+            assert out["y"][n, m] == _round_f32(exact)
+    p2 = _avg_params(8, 1, np.zeros((8, 16, 1), np.uint8))
+    with pytest.raises(RuntimeError):
+        oracle.amm(p2, np.zeros((1, 8), np.float32), relu=False, summation="avg16")

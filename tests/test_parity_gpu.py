@@ -243,3 +243,29 @@ def test_mlp_cfg4_shapes_sampled(C):
     rows = np.unique(np.concatenate([np.random.default_rng(1).choice(70000, 600, replace=False), [0, 69999]]))
     ref = oracle.mlp_forward(oparams, w["relus"], w["A"][rows])
     assert_out(y[rows], ref)
+
+
+@pytest.mark.parametrize("seed,N,D,M,C,dtype", [(21, 1000, 64, 40, 16, "f32"), (22, 777, 200, 300, 32, "f32"),
+                                                (23, 1500, 512, 96, 64, "bf16"), (24, 300, 1024, 48, 256, "f32")])
+def test_parity_avg16(seed, N, D, M, C, dtype):
+    """avg16 summation (reading R22) on the CUDA-core kernels: codes, group-average sums and fp32
+    outputs bit-exact vs the oracle, fused and two-step; the exact plan is unaffected."""
+    from paper_2207_05808_b200 import Plan
+    w = synth.small_case(seed, N=N, D=D, M=M, C=C, dtype=dtype, n_train=600)
+    params = ofit.fit(w["A_train"], w["B"], C, w["perm"], w["bias"], a_is_bf16=dtype == "bf16")
+    ref = oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, want_acc=True, nthreads=8, summation="avg16")
+    plan = Plan(params)
+    plan.set_summation("avg16")
+    Ad = _dev(w["A"], dtype)
+    y = plan.amm(Ad, relu=w["relu"])
+    codes = plan.encode(Ad)
+    acc = torch.empty((N, M), dtype=torch.int32, device="cuda")
+    y2, _ = plan.lut_accumulate(codes, acc=acc, relu=w["relu"])
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref["acc"])
+    assert_out(y.cpu().numpy(), ref["y"])
+    assert_out(y2.cpu().numpy(), ref["y"])
+    plan.set_summation("exact")
+    ye = plan.amm(Ad, relu=w["relu"])
+    torch.cuda.synchronize()
+    assert_out(ye.cpu().numpy(), oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, nthreads=8)["y"])
