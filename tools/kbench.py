@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--only", default="encode,acc,fused")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--summation", default="exact")
     args = ap.parse_args()
     global GRAPH
     GRAPH = not args.no_graph
@@ -64,6 +65,8 @@ def main():
     w = synth.workload(args.workload, n_rows=n)
     params = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
     plan = Plan(params)
+    if args.summation != "exact":
+        plan.set_summation(args.summation)
     A = torch.from_numpy(w["A"].view(np.int16) if bf16 else w["A"]).cuda()
     if bf16:
         A = A.view(torch.bfloat16)
