@@ -20,6 +20,7 @@
 #include "simt.cuh"
 #include "tc.cuh"
 #include "sp.cuh"
+#include "tc2.cuh"
 
 using namespace itlumm;
 
@@ -515,7 +516,9 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
     TcArgs a{};
     a.A = A; a.lda = lda; a.codes = codes; a.ldc = ldc; a.N = N; a.acc = acc; a.ldacc = ldacc;
     a.out = out; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
-    itlumm_status st = tc_launch(P->tc, P->dp, fused, dtype == ITLUMM_BF16, a, s);
+    bool launched = false;
+    itlumm_status st = fused ? ITLUMM_OK : tc2_launch(P->tc, P->dp, a, s, P->num_sms, false, &launched);
+    if (st == ITLUMM_OK && !launched) st = tc_launch(P->tc, P->dp, fused, dtype == ITLUMM_BF16, a, s);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     g_launches = 1;
     return ITLUMM_OK;
@@ -570,7 +573,9 @@ static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtyp
     TcArgs a{};
     a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;
     a.out = out + (size_t)r0 * ldo; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
-    st = tc_launch(P->tc, P->dp, false, false, a, s, true);
+    bool launched = false;
+    st = tc2_launch(P->tc, P->dp, a, s, P->num_sms, true, &launched);
+    if (st == ITLUMM_OK && !launched) st = tc_launch(P->tc, P->dp, false, false, a, s, true);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     launches += 2;
   }

@@ -269,3 +269,27 @@ def test_parity_avg16(seed, N, D, M, C, dtype):
     ye = plan.amm(Ad, relu=w["relu"])
     torch.cuda.synchronize()
     assert_out(ye.cpu().numpy(), oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, nthreads=8)["y"])
+
+
+def test_parity_cta_pair_kernel_streamed_lut(monkeypatch):
+    """The cta_group::2 pair kernel (k_tc2, opt-in ITLUMM_TC2=1) on streamed LUTs: bit-exact vs the
+    oracle (run in a subprocess so the opt-in flag is read at library load)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, synth, oracle\n"
+        "from oracle import fit as ofit\n"
+        "from paper_2207_05808_b200 import Plan\n"
+        "for seed, N, D, M, C, dt in [(10, 3000, 4096, 512, 256, 'bf16'), (14, 700, 2048, 300, 512, 'f32')]:\n"
+        "    w = synth.small_case(seed, N=N, D=D, M=M, C=C, dtype=dt, n_train=600)\n"
+        "    p = ofit.fit(w['A_train'], w['B'], C, w['perm'], w['bias'], a_is_bf16=dt == 'bf16')\n"
+        "    ref = oracle.amm(p, w['A'], relu=w['relu'], dtype=dt, nthreads=8)['y']\n"
+        "    A = torch.from_numpy(w['A'].view(np.int16) if dt == 'bf16' else w['A']).cuda()\n"
+        "    A = A.view(torch.bfloat16) if dt == 'bf16' else A\n"
+        "    y = Plan(p).amm(A, relu=w['relu']).cpu().numpy()\n"
+        "    assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), seed\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, ITLUMM_TC2="1", PYTHONPATH=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
