@@ -83,6 +83,7 @@ struct TcKArgs {
   // so its K-blocks stream from L2); each stage carries the one-hot K-block and the LUT K-block.
   int stream_b;
   int ST;          // ring stages
+  int BST;         // k_tc2: LUT-half ring stages
   uint64_t* trace; // developer timeline (ITLUMM_TC_TRACE): [8 CTAs][4 roles][kTraceEv] globaltimer stamps
 };
 constexpr int kTraceEv = 512;

@@ -20,8 +20,9 @@
 
 namespace itlumm {
 
-constexpr int kTc2Threads = kTcThreads + 32;      // + forwarder warp
+constexpr int kTc2Threads = kTcThreads + 64;      // + LUT forwarder warp + one-hot forwarder warp
 constexpr int kTc2FwdWarp = kTcLoaderWarp + 1;    // warp 14
+constexpr int kTc2AFwdWarp = kTcLoaderWarp + 2;   // warp 15
 constexpr int kTc2Stages = 4;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -62,16 +63,17 @@ __host__ __device__ constexpr uint32_t idesc_i8_m256(int n) {
 struct Tc2Smem {
   size_t b, a, stg, codes, bar, tmem, total;
 };
-// per CTA: ST stages of (half LUT K-block: 128 columns x 128 B) + (one-hot K-block: 128 rows x 128 B)
-__host__ __device__ inline Tc2Smem tc2_smem_layout(int CS, int ldc, int ST = kTc2Stages) {
+// per CTA: a ring of ST one-hot K-blocks (128 rows x 128 B) and a deeper ring of BST half LUT
+// K-blocks (128 columns x 128 B): the LUT halves ride the longer L2 -> forwarder -> leader path.
+__host__ __device__ inline Tc2Smem tc2_smem_layout(int CS, int ldc, int ST = kTc2Stages, int BST = kTc2Stages) {
   Tc2Smem s{};
   size_t o = 0;
-  s.b = o;     o += (size_t)ST * 128 * kKBlock;
+  s.b = o;     o += (size_t)BST * 128 * kKBlock;
   s.a = o;     o += (size_t)ST * kTcRows * kKBlock;
   s.stg = o;   o += (size_t)kTcEpiWarps * kTcStage;
   s.codes = o; o += (size_t)CS * kTcRows * ldc;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;   o += (size_t)(4 * ST + 4 + 2 * CS) * 8;
+  s.bar = o;   o += (size_t)(3 * ST + 4 * BST + 4 + 2 * CS) * 8;
   s.tmem = o;  o += 16;
   s.total = o + 1024;
   return s;
@@ -81,16 +83,19 @@ __host__ __device__ inline Tc2Smem tc2_smem_layout(int CS, int ldc, int ST = kTc
 __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_raw2[];
   uint8_t* smem = smem_raw2 + ((1024u - (smem_u32(smem_raw2) & 1023u)) & 1023u);
-  const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, CS = g.CS, ST = g.ST;
-  const Tc2Smem L = tc2_smem_layout(CS, (int)g.ldc, ST);
+  const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, CS = g.CS, ST = g.ST, BST = g.BST;
+  const Tc2Smem L = tc2_smem_layout(CS, (int)g.ldc, ST, BST);
   uint8_t* b_s = smem + L.b;
   uint8_t* a_s = smem + L.a;
   uint8_t* codes_s = smem + L.codes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar);   // leader: 2x128 producers + 2 forwards
-  uint64_t* empty_bar = full_bar + ST;                                // multicast MMA commit
-  uint64_t* bfull_bar = empty_bar + ST;                               // local: LUT half landed
-  uint64_t* bfwd_bar = bfull_bar + ST;                                // local: forwarder done with stage
-  uint64_t* accf_bar = bfwd_bar + ST;                                 // multicast MMA commit
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar);   // leader: one-hot of both CTAs (2)
+  uint64_t* empty_bar = full_bar + ST;                                // multicast MMA commit (one-hot)
+  uint64_t* bready_bar = empty_bar + ST;                              // leader: LUT halves of both CTAs (2)
+  uint64_t* bempty_bar = bready_bar + BST;                            // multicast MMA commit (LUT)
+  uint64_t* bfull_bar = bempty_bar + BST;                             // local: LUT half landed
+  uint64_t* bfwd_bar = bfull_bar + BST;                               // local: forwarder done with stage
+  uint64_t* afull_bar = bfwd_bar + BST;                               // local: 128 producers wrote the stage
+  uint64_t* accf_bar = afull_bar + ST;                                // multicast MMA commit
   uint64_t* acce_bar = accf_bar + 2;                                  // leader: 2 x 256 epilogue threads
   uint64_t* codes_bar = acce_bar + 2;
   uint64_t* codes_empty = codes_bar + CS;
@@ -116,8 +121,13 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(full_bar + s, 4);                 // 2 producer groups + 2 forwarders
+      mbar_init(full_bar + s, 2);                 // the one-hot forwarders of the pair
       mbar_init(empty_bar + s, 1);
+      mbar_init(afull_bar + s, kTcProducers);
+    }
+    for (int s = 0; s < BST; ++s) {
+      mbar_init(bready_bar + s, 2);               // the 2 forwarders of the pair
+      mbar_init(bempty_bar + s, 1);
       mbar_init(bfull_bar + s, 1);
       mbar_init(bfwd_bar + s, 1);
     }
@@ -136,6 +146,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
   const uint32_t tmem_base = *tmem_slot;
   if (g.pdl) pdl_wait();
   const uint32_t full_leader = mapa_shared(smem_u32(full_bar), 0);
+  const uint32_t bready_leader = mapa_shared(smem_u32(bready_bar), 0);
   const uint32_t acce_leader = mapa_shared(smem_u32(acce_bar), 0);
 
   if (warp == kTcLoaderWarp) {
@@ -155,11 +166,11 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
         if (++cs == CS) { cs = 0; cph ^= 1; }
         const uint8_t* src = g.qt + ((size_t)sl * KB * NS + (size_t)rank * 128) * kKBlock;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(empty_bar + stage, phase ^ 1);                  // pair's MMAs done with the stage
+          mbar_wait(bempty_bar + stage, phase ^ 1);                 // pair's MMAs done with the stage
           mbar_wait(bfwd_bar + stage, phase ^ 1);                   // forwarder saw the previous fill
           mbar_arrive_expect_tx(bfull_bar + stage, hbytes);
           bulk_g2s(b_s + (size_t)stage * hbytes, src + (size_t)kb * NS * kKBlock, hbytes, bfull_bar + stage);
-          if (++stage == ST) { stage = 0; phase ^= 1; }
+          if (++stage == BST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -173,9 +184,23 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
       for (int64_t k = 0; item(k, tile, sl); ++k)
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(bfull_bar + stage, phase);
-          mbar_arrive_cluster(full_leader + stage * 8);
+          mbar_arrive_cluster(bready_leader + stage * 8);
           stamp(3);
           mbar_arrive(bfwd_bar + stage);
+          if (++stage == BST) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp == kTc2AFwdWarp) {
+    // ======================================================== one-hot forwarder: stage -> leader
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k)
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(afull_bar + stage, phase);
+          mbar_arrive_cluster(full_leader + stage * 8);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
     }
@@ -203,15 +228,12 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
           *reinterpret_cast<uint4*>(st + sw128_off(r, j)) =
               make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
         }
-        // every producer fences its one-hot stores for the tensor cores, the group meets at a
-        // named barrier, and ONE cluster-scope arrival per CTA tells the leader (a cluster-scope
-        // release per thread per K-block is far too slow)
+        // producers release their one-hot stores locally (CTA scope); the one-hot forwarder warp
+        // turns each completed stage into one cluster-scope arrival on the leader, off the
+        // producers' critical path
         fence_proxy_async_smem();
-        named_bar_sync(2, kTcProducers);
-        if (r == 0) {
-          mbar_arrive_cluster(full_leader + stage * 8);
-          stamp(0);
-        }
+        mbar_arrive(afull_bar + stage);
+        if (r == 0) stamp(0);
         if (++stage == ST) { stage = 0; phase ^= 1; }
       }
       mbar_arrive(codes_empty + cs);
@@ -221,8 +243,8 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
     // ======================================================== MMA: leader CTA issues for the pair
     if (rank == 0) {
       const uint32_t idesc = idesc_i8_m256(NS);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
+      int stage = 0, acc = 0, bstage = 0;
+      uint32_t phase = 0, acc_phase = 0, bphase = 0;
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
@@ -231,20 +253,23 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_tc2(DevPlan p, TcKArgs g, co
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(full_bar + stage, phase);
+          mbar_wait(bready_bar + bstage, bphase);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kTcRows * kKBlock);
-            const uint32_t b_addr = smem_u32(b_s + (size_t)stage * 128 * kKBlock);
+            const uint32_t b_addr = smem_u32(b_s + (size_t)bstage * 128 * kKBlock);
 #pragma unroll
             for (int ks = 0; ks < kKBlock / 32; ++ks)
               umma_i8_2sm(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
                           (kb | ks) != 0);
             umma_commit_2sm(empty_bar + stage);
+            umma_commit_2sm(bempty_bar + bstage);
             if (kb == KB - 1) umma_commit_2sm(accf_bar + acc);
             stamp(1);
           }
           __syncwarp();
           if (++stage == ST) { stage = 0; phase ^= 1; }
+          if (++bstage == BST) { bstage = 0; bphase ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
@@ -325,11 +350,11 @@ namespace itlumm {
 
 // Launch k_tc2 for a streamed-LUT plan when it applies (codes path, TMA-storable output, no int32
 // acc output, 256-column slices, 16-byte codes rows).  Returns false (nothing launched) otherwise.
-// OFF by default: measured slower than the 1-CTA streamed kernel (cfg3 C=128: 156 vs 101 us; the
-// K-block cadence is ~700-800 ns, bound by the cross-CTA round trip of the 4-stage ring: LUT half
-// lands -> forwarder -> leader's full barrier -> MMA -> multicast commit -> refill; a cluster-scope
-// release per K-block costs ~0.3 us more than a CTA-scope one).  Parity-exact; opt in with
-// ITLUMM_TC2=1 (developer knob, not ABI).
+// OFF by default: measured slower than the 1-CTA streamed kernel (cfg3 C=64 / C=128 / cfg5:
+// 83 / 140 / 5090 us vs 61 / 101 / 3560 us).  With the one-hot and LUT rings decoupled and their
+// cluster-scope arrivals moved to forwarder warps, the K-block cadence settles at ~650 ns for any
+// ring depth from 3 to 7 (profiles/r01/tc2_stage_sweep.txt), i.e. a throughput limit of the pair
+// MMA path rather than latency.  Parity-exact; opt in with ITLUMM_TC2=1 (developer knob, not ABI).
 inline bool tc2_applicable(const TcPlan& t, const TcArgs& a) {
   static const bool on = getenv("ITLUMM_TC2") && atoi(getenv("ITLUMM_TC2")) != 0;
   return on && t.stream_b && t.NS == 256 && t.tmem_cols == 512 && !a.acc && a.out && a.ldc % 16 == 0 &&
@@ -343,13 +368,19 @@ inline itlumm_status tc2_launch(const TcPlan& t, const DevPlan& dp, const TcArgs
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
   if (!make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) return ITLUMM_OK;
-  int CS = 0;
-  size_t smem = 0;
-  for (int cs = 4; cs >= 1; --cs) {
-    const size_t need = tc2_smem_layout(cs, (int)a.ldc).total;
-    if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { CS = cs; smem = need; break; }
+  // one-hot and LUT-half rings of similar depth (the cross-CTA round trip is long on both), 2 codes
+  // stages (1 if short of room).  Developer override (not ABI): ITLUMM_TC2_ST.
+  static const int st_env = getenv("ITLUMM_TC2_ST") ? atoi(getenv("ITLUMM_TC2_ST")) : 0;
+  int ST = (st_env >= 2 && st_env <= 8) ? st_env : 5;
+  int CS = 2, BST = 0;
+  if (tc2_smem_layout(CS, (int)a.ldc, ST, 4).total > kSmemMax) CS = 1;
+  while (BST < 8 && tc2_smem_layout(CS, (int)a.ldc, ST, BST + 1).total <= kSmemMax) ++BST;
+  while (BST < 3 && ST > 2) {
+    --ST;
+    while (BST < 8 && tc2_smem_layout(CS, (int)a.ldc, ST, BST + 1).total <= kSmemMax) ++BST;
   }
-  if (CS == 0) return ITLUMM_OK;
+  if (BST < 2 || (int64_t)kTcRows * a.ldc >= (1 << 20)) return ITLUMM_OK;
+  const size_t smem = tc2_smem_layout(CS, (int)a.ldc, ST, BST).total;
   static bool attr_done = false;
   if (!attr_done) {
     if (cudaFuncSetAttribute((const void*)k_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) != cudaSuccess)
@@ -359,7 +390,7 @@ inline itlumm_status tc2_launch(const TcPlan& t, const DevPlan& dp, const TcArgs
   TcKArgs k{};
   k.codes = a.codes; k.ldc = a.ldc; k.N = a.N; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
-  k.CS = CS; k.pdl = pdl ? 1 : 0; k.tma_store = 1; k.ST = kTc2Stages; k.stream_b = 1;
+  k.CS = CS; k.pdl = pdl ? 1 : 0; k.tma_store = 1; k.ST = ST; k.BST = BST; k.stream_b = 1;
   k.trace = t.trace;
   const int64_t units = ((a.N + 255) / 256) * t.G;
   int64_t pairs = num_sms / 2;
