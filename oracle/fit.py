@@ -146,3 +146,48 @@ def fit(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray, bias: np.n
                 thresholds=thresholds, lut=q, scale=scale_f, offset=lo_f,
                 bias=np.asarray(bias, dtype=np.float32).copy(),
                 T=T, scale64=scale, lo64=lo, prototypes=P_all, leaf_sizes=leaf_sizes)
+
+
+def onehot(codes: np.ndarray) -> np.ndarray:
+    """G: the concatenation of C one-hot 16-dimensional vectors per row, N x 16C, fp64."""
+    N, C = codes.shape
+    G = np.zeros((N, K * C), dtype=np.float64)
+    for c in range(C):
+        G[np.arange(N), K * c + codes[:, c].astype(np.int64)] = 1.0
+    return G
+
+
+def optimize_lut_linear(A: np.ndarray, B: np.ndarray, codes: np.ndarray, T0: np.ndarray, lam: float) -> np.ndarray:
+    """ITLUMM model-aware LUT optimisation, Eq. 3, for sigma = the bias alone (no
+    nonlinearity): argmin_T ||A B - G T||^2 + lam ||T - P0 B||^2 (the bias cancels inside the
+    norm).  Normal equations (G^T G + lam I) T = G^T (A B) + lam P0 B, solved in fp64.
+    A: N x D training rows, B: D x M, codes: N x C, T0 = P0 B as [C][16][M].  Returns [C][16][M]."""
+    C = codes.shape[1]
+    M = B.shape[1]
+    G = onehot(codes)
+    Y = np.asarray(A, np.float64) @ np.asarray(B, np.float64)
+    T0f = np.asarray(T0, np.float64).reshape(K * C, M)
+    lhs = G.T @ G + lam * np.eye(K * C)
+    rhs = G.T @ Y + lam * T0f
+    return np.linalg.solve(lhs, rhs).reshape(C, K, M)
+
+
+def eq3_objective(A, B, bias, codes, T, T0, lam, relu: bool) -> float:
+    """||sigma(A B) - sigma(G T)||^2 + lam ||T - P0 B||^2 with sigma = (+ bias) then ReLU if relu."""
+    G = onehot(codes)
+    C = codes.shape[1]
+    M = B.shape[1]
+    Y = np.asarray(A, np.float64) @ np.asarray(B, np.float64) + np.asarray(bias, np.float64)
+    Z = G @ np.asarray(T, np.float64).reshape(K * C, M) + np.asarray(bias, np.float64)
+    if relu:
+        Y, Z = np.maximum(Y, 0), np.maximum(Z, 0)
+    return float(((Y - Z) ** 2).sum() + lam * ((np.asarray(T) - np.asarray(T0)) ** 2).sum())
+
+
+def requantize(params: dict, T: np.ndarray) -> dict:
+    """Same trees, LUT from table T through the same uint8 quantiser (reading R6)."""
+    q, scale, lo = quantize(np.asarray(T, np.float64))
+    out = dict(params)
+    out.update(lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32), T=np.asarray(T, np.float64),
+               scale64=scale, lo64=lo)
+    return out

@@ -104,13 +104,21 @@ def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | Non
         Bc = Bp[bnd[c]:bnd[c + 1]]
         for j in range(P.shape[1]):
             T[c] += P[:, j:j + 1] * Bc[j:j + 1, :]
+    q, scale, lo = quantize_table(T)
+    return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr,
+                lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
+                bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)), T=T)
+
+
+def quantize_table(T: np.ndarray):
+    """uint8 LUT with per-output-column scale/offset (reading R6): lo = min, scale = (hi-lo)/255
+    (1 for a constant column), q = clamp(floor((T-lo)/scale + 0.5), 0, 255), fp64."""
+    T = np.asarray(T, np.float64)
     lo = T.min(axis=(0, 1))
     hi = T.max(axis=(0, 1))
     scale = np.where(hi > lo, (hi - lo) / 255.0, 1.0)
     q = np.clip(np.floor((T - lo) / scale + 0.5), 0, 255).astype(np.uint8)
-    return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr,
-                lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
-                bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)))
+    return q, scale, lo
 
 
 def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, relus: list,
@@ -136,4 +144,55 @@ def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, 
                 At = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(f"cuda:{device}")
             X = plan.amm(At, relu=relu).cpu().numpy()
             plan.close()
+    return out
+
+
+def optimize_lut(params: dict, A_train: np.ndarray, B: np.ndarray, lam: float = 1.0, relu: bool = False,
+                 iters: int = 200, lr: float = 1e-2, device: int = 0, a_is_bf16: bool = False) -> dict:
+    """ITLUMM model-aware LUT optimisation, Eq. 3, on the GPU:
+    argmin_T ||sigma(A B) - sigma(G T)||^2 + lam ||T - P0 B||^2, sigma = + bias (then ReLU when
+    `relu`).  G comes from the plan's own encode kernel on the training rows.  Without a
+    nonlinearity the bias cancels and T solves the normal equations (G^T G + lam I) T = G^T A B +
+    lam P0 B (fp64, cuSOLVER through torch.linalg); with ReLU that solution seeds `iters` Adam steps
+    on the ReLU objective.  Returns the parameters with the new table requantised (same trees), so
+    the hot path is unchanged."""
+    import torch
+    from .api import Plan
+
+    dev = torch.device("cuda", device)
+    C, M = int(params["C"]), int(params["M"])
+    plan = Plan(params, device=device)
+    X = np.asarray(A_train)
+    if a_is_bf16:
+        At = torch.from_numpy(np.ascontiguousarray(X).view(np.int16)).to(dev).view(torch.bfloat16)
+        Af = torch.from_numpy((X.astype(np.uint32) << 16).view(np.float32)).to(dev).double()
+    else:
+        At = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(dev)
+        Af = At.double()
+    packed = plan.encode(At)
+    plan.close()
+    lo_nib, hi_nib = packed & 15, packed >> 4
+    codes = torch.stack([lo_nib, hi_nib], dim=2).reshape(packed.shape[0], -1)[:, :C].long()
+    N = codes.shape[0]
+    G = torch.zeros((N, 16 * C), dtype=torch.float64, device=dev)
+    G.scatter_(1, codes + 16 * torch.arange(C, device=dev), 1.0)
+    Y = Af @ torch.from_numpy(np.asarray(B, np.float64)).to(dev)
+    T0 = torch.from_numpy(np.asarray(params["T"], np.float64).reshape(16 * C, M)).to(dev)
+    lhs = G.T @ G + lam * torch.eye(16 * C, dtype=torch.float64, device=dev)
+    T = torch.linalg.solve(lhs, G.T @ Y + lam * T0)
+    if relu:
+        b = torch.from_numpy(np.asarray(params["bias"], np.float64)).to(dev)
+        target = torch.relu(Y + b)
+        Tv = T.clone().requires_grad_(True)
+        opt = torch.optim.Adam([Tv], lr=lr)
+        for _ in range(int(iters)):
+            opt.zero_grad()
+            loss = ((target - torch.relu(G @ Tv + b)) ** 2).sum() / N + lam * ((Tv - T0) ** 2).sum() / N
+            loss.backward()
+            opt.step()
+        T = Tv.detach()
+    Tn = T.reshape(C, 16, M).cpu().numpy()
+    q, scale, lo = quantize_table(Tn)
+    out = dict(params)
+    out.update(lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32), T=Tn)
     return out

@@ -441,3 +441,45 @@ def test_avg16_dequant_is_one_rounding_and_rejects_ragged_C():
     p2 = _avg_params(8, 1, np.zeros((8, 16, 1), np.uint8))
     with pytest.raises(RuntimeError):
         oracle.amm(p2, np.zeros((1, 8), np.float32), relu=False, summation="avg16")
+
+
+# ---------------------------------------------------------------------------- f4: Eq. 3 LUT fit
+def test_eq3_linear_single_codebook_is_bucket_ridge_mean():
+    """C = 1: G^T G is diagonal (bucket counts), so Eq. 3 with sigma = bias reduces per code k to
+    T[k] = (sum of the targets a.B of the rows in bucket k + lam T0[k]) / (count_k + lam)."""
+    rng = np.random.default_rng(3)
+    N, D, M, lam = 400, 6, 5, 2.5
+    A = rng.normal(size=(N, D))
+    B = rng.normal(size=(D, M))
+    codes = rng.integers(0, 16, size=(N, 1)).astype(np.uint8)
+    T0 = rng.normal(size=(1, 16, M))
+    T = ofit.optimize_lut_linear(A, B, codes, T0, lam)
+    Y = A @ B
+    for k in range(16):
+        rows = codes[:, 0] == k
+        want = (Y[rows].sum(axis=0) + lam * T0[0, k]) / (rows.sum() + lam)
+        assert np.allclose(T[0, k], want, rtol=1e-12, atol=1e-12)
+
+
+def test_eq3_linear_optimality_and_limits():
+    """The solution satisfies the normal equations, is no worse than P0 B for the objective, and
+    tends to P0 B as lam grows."""
+    rng = np.random.default_rng(4)
+    N, D, M, C = 600, 24, 7, 4
+    A = rng.normal(size=(N, D))
+    B = rng.normal(size=(D, M))
+    bias = rng.normal(size=M)
+    codes = rng.integers(0, 16, size=(N, C)).astype(np.uint8)
+    T0 = rng.normal(size=(C, 16, M))
+    T = ofit.optimize_lut_linear(A, B, codes, T0, 0.3)
+    G = ofit.onehot(codes)
+    resid = (G.T @ G + 0.3 * np.eye(16 * C)) @ T.reshape(-1, M) - (G.T @ (A @ B) + 0.3 * T0.reshape(-1, M))
+    assert np.abs(resid).max() < 1e-8
+    f = lambda TT: ofit.eq3_objective(A, B, bias, codes, TT, T0, 0.3, relu=False)  # noqa: E731
+    assert f(T) <= f(T0) + 1e-9
+    for d in (1e-3, -1e-3):
+        Tp = T.copy()
+        Tp[1, 3, 2] += d
+        assert f(T) <= f(Tp)
+    Tbig = ofit.optimize_lut_linear(A, B, codes, T0, 1e9)
+    assert np.abs(Tbig - T0).max() < 1e-5

@@ -293,3 +293,28 @@ def test_parity_cta_pair_kernel_streamed_lut(monkeypatch):
     env = dict(os.environ, ITLUMM_TC2="1", PYTHONPATH=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_eq3_lut_optimisation_gpu_vs_oracle():
+    """f4 (Eq. 3): the GPU fit's linear solution equals the oracle's fp64 normal-
+    equation solution; the ReLU refinement lowers the ReLU objective; the requantised layer keeps
+    kernel/oracle parity (only LUT values change) and reconstructs sigma(A B) at least as well
+    as the prototype table on the training rows."""
+    from paper_2207_05808_b200 import Plan, fit_layer
+    from paper_2207_05808_b200.fit import optimize_lut
+    w = synth.small_case(41, N=2000, D=96, M=24, C=8, n_train=1500)
+    p = fit_layer(w["A_train"], w["B"], 8, w["perm"], w["bias"])
+    po = ofit.fit(w["A_train"], w["B"], 8, w["perm"], w["bias"])       # the oracle's own fit
+    lin = optimize_lut(p, w["A_train"], w["B"], lam=0.5)
+    op = oracle.amm(po, w["A_train"], relu=False, want_codes=True, nthreads=8)
+    Tref = ofit.optimize_lut_linear(w["A_train"], w["B"], op["codes"], po["T"], 0.5)
+    assert np.allclose(lin["T"], Tref, rtol=1e-7, atol=1e-9)
+    obj = lambda T, relu: ofit.eq3_objective(w["A_train"], w["B"], w["bias"], op["codes"], T, po["T"], 0.5, relu)  # noqa: E731
+    assert obj(lin["T"], False) <= obj(po["T"], False)
+    rel = optimize_lut(p, w["A_train"], w["B"], lam=0.5, relu=True, iters=100)
+    assert obj(rel["T"], True) <= obj(lin["T"], True) + 1e-6
+    plan = Plan(rel)
+    y = plan.amm(torch.from_numpy(w["A"]).cuda(), relu=True)
+    torch.cuda.synchronize()
+    rel_o = ofit.requantize(po, rel["T"])      # oracle params: its own trees + the fitted table
+    assert_out(y.cpu().numpy(), oracle.amm(rel_o, w["A"], relu=True, nthreads=8)["y"])
