@@ -119,6 +119,12 @@ __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t v) {
   }
 }
 
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ float relu_pos0(float y) { return y > 0.0f ? y : 0.0f; }
 
 __device__ __forceinline__ void st_cs_f4(float* p, float a, float b, float c, float d) {

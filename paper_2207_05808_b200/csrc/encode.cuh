@@ -30,6 +30,7 @@ struct EncArgs {
   int row_bytes;        // bytes of one staged row (D * es, multiple of 16)
   int contiguous;       // lda == D: a tile is one bulk copy
   int pdl;              // let a dependent grid launch early (PDL)
+  uint64_t* span;       // developer trace: [cta][2] globaltimer at CTA start / end (or null)
 };
 
 // Shared-memory footprint: [S][R][row_bytes] rows | cols [C][4] | thr [15][C] | 2S mbarriers.
@@ -64,6 +65,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   const char* A = reinterpret_cast<const char*>(g.A);
   const size_t ldab = (size_t)g.lda * sizeof(T);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (g.span && threadIdx.x == 0) g.span[2 * cta] = gtimer_ns();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, nconsumer); mbar_init(pub + s, 1); }
@@ -152,6 +154,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);             // releases this warp's code stores (CTA scope)
   }
+  if (g.span && cw == 0 && lane == 0) g.span[2 * cta + 1] = gtimer_ns();
 }
 
 template <typename T>

@@ -310,8 +310,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
   if (st == ITLUMM_OK && getenv("ITLUMM_TC_TRACE") && atoi(getenv("ITLUMM_TC_TRACE")) != 0) {
-    cudaMalloc(&P->tc.trace, (size_t)16 * 4 * kTraceEv * 8);
-    if (P->tc.trace) cudaMemset(P->tc.trace, 0, (size_t)16 * 4 * kTraceEv * 8);
+    cudaMalloc(&P->tc.trace, ((size_t)16 * 4 * kTraceEv + 4 * 512) * 8);
+    if (P->tc.trace) cudaMemset(P->tc.trace, 0, ((size_t)16 * 4 * kTraceEv + 4 * 512) * 8);
   }
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
   if (P->tc.ok) {
@@ -455,6 +455,7 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
       g.R = R; g.S = S; g.row_bytes = (int)rb; g.contiguous = lda == P->D; g.pdl = pdl ? 1 : 0;
+      g.span = P->tc.trace ? P->tc.trace + (size_t)16 * 4 * kTraceEv : nullptr;
       const int64_t ntiles = (N + R - 1) / R;
       const unsigned grid = (unsigned)std::min<int64_t>(ntiles, P->num_sms);
       const size_t smem = enc_smem_bytes(P->C, R, S, (int)rb);
@@ -933,7 +934,7 @@ extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_
 // starts and K-block commits, epilogue warp-0 tile start/end, codes loads); copy them out here.
 extern "C" int itlumm_dbg_trace_copy(itlumm_plan P, uint64_t* host, int64_t n) {
   if (!P || !P->tc.trace || !host) return 1;
-  const int64_t total = (int64_t)16 * 4 * kTraceEv;
+  const int64_t total = (int64_t)16 * 4 * kTraceEv + 4 * 512;
   cudaDeviceSynchronize();
   return cudaMemcpy(host, P->tc.trace, (size_t)std::min(n, total) * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }

@@ -250,6 +250,9 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* trace = (g.trace && cta < 8) ? g.trace + (size_t)cta * 4 * kTraceEv : nullptr;
+  // per-CTA spans after the role timelines: [16 x 4 x kTraceEv] | encoder [512][2] | TC [512][2]
+  uint64_t* span = (g.trace && cta < 512) ? g.trace + (size_t)16 * 4 * kTraceEv + 2 * 512 + 2 * cta : nullptr;
+  if (span && threadIdx.x == 0) span[0] = gtimer();
   int tev[4] = {0, 0, 0, 0};
   auto stamp = [&](int role) {                          // role: 0 producer, 1 MMA, 2 epilogue, 3 loader
     if (trace && tev[role] < kTraceEv) trace[role * kTraceEv + tev[role]++] = gtimer();
@@ -683,6 +686,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
 
   tc_fence_before();
   __syncthreads();
+  if (span && threadIdx.x == 0) span[1] = gtimer();
   if (warp == kTcMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(g.tmem_cols) : "memory");
