@@ -51,8 +51,8 @@ typedef enum { ITLUMM_F32 = 0, ITLUMM_BF16 = 1 } itlumm_dtype;            /* ele
 typedef enum { ITLUMM_EPI_NONE = 0, ITLUMM_EPI_RELU = 1 } itlumm_epilogue;  /* sigma    */
 
 /* Kernel schedule used by itlumm_amm / itlumm_amm_host / itlumm_lut_accumulate.
- *   AUTO    : library choice: TC_PIPE when the tensor-core
- *             tiling splits M over several CTAs, else TC; SIMT where TC does not apply.
+ *   AUTO    : library choice: TC_PIPE (itlumm_amm) / TC
+ *             (itlumm_lut_accumulate) where the tensor-core tiling applies, else SIMT.
  *   SIMT    : CUDA-core shared-memory LUT kernels; itlumm_amm = one fused kernel.
  *   TC      : tcgen05 one-hot x LUT int8 tensor-core kernel (G.T with G the one-hot encoding,
  *             P:89; exact integer products); itlumm_amm = one fused kernel (encode inside).

@@ -69,6 +69,7 @@ struct itlumm_plan_s {
   bool scratch_used = false;
   uint32_t* ready = nullptr;     // [scratch_rows / 128] x 2: TC_SP ready / consumed counters (zeroed)
   bool coop = false;             // device supports cooperative launches
+  double seg_frac[2] = {1.0, 1.0};  // fraction of a row's 64-byte segments the gather touches (f32, bf16)
   // host API staging
   std::mutex host_mu;
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host API: 3-stage copy/compute ring
@@ -242,6 +243,14 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   if (!P) return fail(ITLUMM_ENOMEM, "host allocation failed");
   P->device = cuda_device;
   P->D = v.in_map ? v.D_in : D; P->C = C; P->M = M; P->Mp = (M + 15) & ~15;
+  for (int d = 0; d < 2; ++d) {               // DRAM lines a per-column gather of a row touches
+    const int es = d == 0 ? 4 : 2;
+    const int nseg = (P->D * es + 63) / 64;
+    std::vector<char> hit(nseg, 0);
+    int n = 0;
+    for (int col : cols) { const int sgi = col * es / 64; if (!hit[sgi]) { hit[sgi] = 1; ++n; } }
+    P->seg_frac[d] = (double)n / nseg;
+  }
   const int Mp = P->Mp;
 
   // host images of the device parameters
@@ -449,8 +458,11 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
   const int es = dtype == ITLUMM_BF16 ? 2 : 4;
   const int64_t rb = (int64_t)P->D * es;
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
+  // Stream whole rows when the split columns touch most of a row's DRAM lines (cfg2: 98%); gather
+  // the columns per thread when they touch few of them (cfg4 C=16 layer 1: 64 of 3072 columns).
+  const bool sparse_cols = P->seg_frac[dtype == ITLUMM_BF16 ? 1 : 0] < 0.6;
   int R = 0, S = 0;
-  if (aligned && enc_tiling(P, rb, kEncConsumerWarps, false, &R, &S)) {
+  if (aligned && !sparse_cols && enc_tiling(P, rb, kEncConsumerWarps, false, &R, &S)) {
     {
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
@@ -505,8 +517,11 @@ static bool use_tc(itlumm_plan P) {
 static bool use_pipe(itlumm_plan P) {
   if (!P->tc.ok || P->summation != ITLUMM_SUM_EXACT) return false;
   if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
-  // a streamed LUT has no fused TC kernel: AUTO pipes it through the encoder
-  return P->algo == ITLUMM_ALGO_AUTO && (P->tc.G > 1 || P->tc.stream_b);
+  // AUTO pipes every tensor-core shape through the streaming encoder: a streamed LUT has no fused
+  // TC kernel, with several slices a fused kernel would repeat the gather per slice, and even with
+  // one slice the fused kernel's per-thread gather is latency-bound (cfg1: 10.0 us fused vs 6.6 us
+  // encode + accumulate)
+  return P->algo == ITLUMM_ALGO_AUTO;
 }
 
 static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm_dtype dtype, int64_t lda,

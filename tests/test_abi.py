@@ -101,3 +101,16 @@ def test_no_cpu_fallback_in_product_path():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "import oracle" not in src and "from oracle" not in src, fn
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/itlumm.h compiles as C99 and the library links from C (no torch, no GPU)."""
+    import subprocess
+    exe = str(tmp_path / "c_abi_smoke")
+    lib_dir = os.path.dirname(_lib.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c_abi_smoke.c"), "-L", lib_dir, "-litlumm",
+                        f"-Wl,-rpath,{lib_dir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("ok 3"), (r.returncode, r.stdout, r.stderr)
