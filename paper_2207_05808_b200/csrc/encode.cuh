@@ -126,7 +126,14 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   }
 
   const int cw = warp - (ready ? 2 : 1);
+  // lanes per row: the codebooks of a row (rounded up to a power of two, >= 2 so that adjacent
+  // lanes pair their nibbles, <= 32); a warp unit covers 32 / lpr rows (short rows, small C) or one
+  // 32-codebook group of one row (C > 32)
+  int lpr = 2;
+  while (lpr < C && lpr < 32) lpr <<= 1;
+  const int rpu = 32 / lpr;                            // rows per warp unit
   const int ngrp = (C + 31) >> 5;                      // 32-codebook groups per row
+  const int rsub = lane / lpr, cl = lane - rsub * lpr;
   int k = 0;
   for (int64_t tile = cta; tile < ntiles; tile += ncta, ++k) {
     const int s = k % S;
@@ -134,22 +141,55 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
     const T* rows = reinterpret_cast<const T*>(rows_s + (size_t)s * R * rb);
     const int64_t r0 = tile * R;
     const int nrows = (int)((g.N - r0) < R ? (g.N - r0) : R);
-    for (int u = cw; u < nrows * ngrp; u += nconsumer) {
-      const int r = u / ngrp, grp = u - r * ngrp;
-      const int c = grp * 32 + lane;
-      const T* a = rows + (size_t)r * rs;
-      uint32_t code = 0;
-      if (c < C) {
-        const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
-        float v[4];
-        v[0] = InTraits<T>::lds(a + col.x);
-        v[1] = InTraits<T>::lds(a + col.y);
-        v[2] = InTraits<T>::lds(a + col.z);
-        v[3] = InTraits<T>::lds(a + col.w);
-        code = (uint32_t)tree_walk(v, thr_s, C, c);
+    const int nunits = ((nrows + rpu - 1) / rpu) * ngrp;
+    if (nunits <= nconsumer) {                         // at most one unit per warp (cfg2 shapes)
+      if (cw < nunits) {
+        const int ur = cw / ngrp, grp = cw - ur * ngrp;
+        const int r = ur * rpu + rsub, c = grp * 32 + cl;
+        uint32_t code = 0;
+        if (r < nrows && c < C) {
+          const T* a = rows + (size_t)r * rs;
+          const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+          float v[4];
+          v[0] = InTraits<T>::lds(a + col.x);
+          v[1] = InTraits<T>::lds(a + col.y);
+          v[2] = InTraits<T>::lds(a + col.z);
+          v[3] = InTraits<T>::lds(a + col.w);
+          code = (uint32_t)tree_walk(v, thr_s, C, c);
+        }
+        const uint32_t hi = __shfl_down_sync(0xffffffffu, code, 1);
+        if (!(lane & 1) && r < nrows && c < C) g.codes[(r0 + r) * g.ldc + (c >> 1)] = (uint8_t)(code | (hi << 4));
       }
-      const uint32_t hi = __shfl_down_sync(0xffffffffu, code, 1);
-      if (!(lane & 1) && c < C) g.codes[(r0 + r) * g.ldc + (c >> 1)] = (uint8_t)(code | (hi << 4));
+    } else
+    // two units per pass: their shared-memory gathers and tree walks overlap
+    for (int u0 = cw; u0 < nunits; u0 += 2 * nconsumer) {
+      uint32_t code[2];
+      int rr[2], cc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = u0 + h * nconsumer;
+        const int ur = u / ngrp, grp = u - ur * ngrp;
+        rr[h] = ur * rpu + rsub;
+        cc[h] = grp * 32 + cl;
+        code[h] = 0;
+        if (u < nunits && rr[h] < nrows && cc[h] < C) {
+          const T* a = rows + (size_t)rr[h] * rs;
+          const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * cc[h]);
+          float v[4];
+          v[0] = InTraits<T>::lds(a + col.x);
+          v[1] = InTraits<T>::lds(a + col.y);
+          v[2] = InTraits<T>::lds(a + col.z);
+          v[3] = InTraits<T>::lds(a + col.w);
+          code[h] = (uint32_t)tree_walk(v, thr_s, C, cc[h]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = u0 + h * nconsumer;
+        const uint32_t hi = __shfl_down_sync(0xffffffffu, code[h], 1);
+        if (u < nunits && !(lane & 1) && rr[h] < nrows && cc[h] < C)
+          g.codes[(r0 + rr[h]) * g.ldc + (cc[h] >> 1)] = (uint8_t)(code[h] | (hi << 4));
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);             // releases this warp's code stores (CTA scope)
