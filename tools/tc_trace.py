@@ -16,8 +16,13 @@ from paper_2207_05808_b200 import Plan, fit_layer, _lib  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 mode = sys.argv[2] if len(sys.argv) > 2 else "acc"      # acc: lut_accumulate; sp: fused TC_SP amm
-cfg = synth.CONFIGS[name]
-w = synth.workload(name, n_rows=cfg["N"])
+if name.startswith("shape:"):                           # shape:N,D,M,C (synthetic small_case)
+    N_, D_, M_, C_ = (int(x) for x in name[6:].split(","))
+    w = synth.small_case(77, N=N_, D=D_, M=M_, C=C_, n_train=2000)
+    cfg = dict(N=N_, M=M_, relu=True, dtype="f32")
+else:
+    cfg = synth.CONFIGS[name]
+    w = synth.workload(name, n_rows=cfg["N"])
 bf16 = cfg["dtype"] == "bf16"
 p = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
 plan = Plan(p, algo="tc" if mode == "acc" else "tc_sp")
@@ -60,4 +65,4 @@ for cta in range(8, 10):
     print("  issue    ", pi[:24].tolist())
     print("  consumed ", cd[:24].tolist())
     print("  publish  ", pu[:24].tolist())
-json.dump(res, open(os.path.join("gpurun_out", f"tc_trace_{name}_{mode}.json"), "w"))
+json.dump(res, open(os.path.join("gpurun_out", f"tc_trace_{name.replace(':', '_').replace(',', '_')}_{mode}.json"), "w"))
