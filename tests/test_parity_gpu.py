@@ -318,3 +318,24 @@ def test_eq3_lut_optimisation_gpu_vs_oracle():
     torch.cuda.synchronize()
     rel_o = ofit.requantize(po, rel["T"])      # oracle params: its own trees + the fitted table
     assert_out(y.cpu().numpy(), oracle.amm(rel_o, w["A"], relu=True, nthreads=8)["y"])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_strided_rows_bulk_copy_path_and_scratch_chunking(dtype):
+    """Rows with lda > D but 16-byte aligned go through the per-row bulk copies of the streaming
+    encoder; N above the plan's 262144-row code scratch runs in chunks; both bit-exact."""
+    from paper_2207_05808_b200 import Plan
+    N, D, M, C = 300001, 32, 24, 8
+    w = synth.small_case(51, N=N, D=D, M=M, C=C, dtype=dtype, n_train=500)
+    params = ofit.fit(w["A_train"], w["B"], C, w["perm"], w["bias"], a_is_bf16=dtype == "bf16")
+    pad = 8                                            # lda = 40 elements: rows stay 16-byte aligned
+    Ah = np.zeros((N, D + pad), np.uint16 if dtype == "bf16" else np.float32)
+    Ah[:, :D] = w["A"]
+    plan = Plan(params)
+    y = plan.amm(_dev(Ah, dtype), relu=True)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    rows = np.unique(np.concatenate([np.random.default_rng(2).choice(N, 3000, replace=False),
+                                     [0, 262143, 262144, N - 1]]))
+    ref = oracle.amm(params, Ah[rows], relu=True, dtype=dtype, nthreads=8)["y"]
+    assert_out(y[rows], ref)
