@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define ITLUMM_ABI_VERSION 3
+#define ITLUMM_ABI_VERSION 4
 
 typedef enum {
   ITLUMM_OK = 0,
@@ -82,6 +82,15 @@ typedef enum {
  *           expected bias per group removed).  CUDA-core kernels only. */
 typedef enum { ITLUMM_SUM_EXACT = 0, ITLUMM_SUM_AVG16 = 1 } itlumm_summation;
 
+/* Operand form of the one-hot matrix G on the tensor-core paths (TC, TC_PIPE).
+ *   DENSE    : G as u8 (16 bytes per codebook), tcgen05.mma kind::i8, K = 32 per instruction.
+ *   SPARSE24 : G is 1-of-16 per codebook, hence 2:4 sparse: stored compressed (8 bytes per
+ *              codebook) with 2-bit position metadata per stored element, tcgen05.mma.sp kind::i8,
+ *              K = 64 per instruction; N slices of at most 224 columns (TMEM holds the metadata).
+ * Both give the same exact integer products (bit-identical results).  TC_SP and the CTA-pair
+ * kernel run DENSE (TC_SP with SPARSE24 runs as TC_PIPE). */
+typedef enum { ITLUMM_ONEHOT_DENSE = 0, ITLUMM_ONEHOT_SPARSE24 = 1 } itlumm_onehot;
+
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */
 
 /* Fitted layer parameters.  HOST pointers, read only during itlumm_plan_create (copied). */
@@ -119,6 +128,10 @@ itlumm_status itlumm_plan_set_algo(itlumm_plan plan, itlumm_algo algo);
  * CUDA-core kernels whatever the algo (acc outputs are then the group-average sums).  Not
  * thread-safe against concurrent launches. */
 itlumm_status itlumm_plan_set_summation(itlumm_plan plan, itlumm_summation summation);
+
+/* Select the one-hot operand form (default DENSE).  EUNSUPPORTED when the tensor-core tiling of
+ * that form does not apply to the plan.  Not thread-safe against concurrent launches. */
+itlumm_status itlumm_plan_set_onehot(itlumm_plan plan, itlumm_onehot onehot);
 
 /* Query plan dims: any out-pointer may be NULL.  lut_bytes = 16*C*M. */
 itlumm_status itlumm_plan_info(itlumm_plan plan, int32_t* D, int32_t* C, int32_t* M,

@@ -15,11 +15,12 @@ F32, BF16 = 0, 1
 EPI_NONE, EPI_RELU = 0, 1
 ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3, "tc_sp": 4}
 SUMMATION = {"exact": 0, "avg16": 1}
+ONEHOT = {"dense": 0, "sparse24": 1}
 
 # every symbol include/itlumm.h declares (checked by tests/test_abi.py against the header)
 EXPORTS = [
     "itlumm_plan_create", "itlumm_plan_destroy", "itlumm_plan_set_algo", "itlumm_plan_set_summation",
-    "itlumm_plan_info",
+    "itlumm_plan_set_onehot", "itlumm_plan_info",
     "itlumm_encode", "itlumm_lut_accumulate", "itlumm_amm", "itlumm_amm_host",
     "itlumm_mlp_create", "itlumm_mlp_destroy", "itlumm_mlp_info", "itlumm_mlp_forward",
     "itlumm_last_launch_count", "itlumm_last_error", "itlumm_abi_version",
@@ -57,6 +58,7 @@ def load():
         "itlumm_plan_destroy": ([V], S),
         "itlumm_plan_set_algo": ([V, S], S),
         "itlumm_plan_set_summation": ([V, S], S),
+        "itlumm_plan_set_onehot": ([V, S], S),
         "itlumm_plan_info": ([V, V, V, V, V], S),
         "itlumm_encode": ([V, V, S, I64, I64, V, I64, V], S),
         "itlumm_lut_accumulate": ([V, V, I64, I64, V, I64, V, I64, S, V], S),

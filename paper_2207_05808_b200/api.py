@@ -66,6 +66,7 @@ class Plan:
         _lib.check(self._lib.itlumm_plan_create(ctypes.byref(p), int(device), ctypes.byref(h)))
         self._h = h
         self.D, self.C, self.M, self.device = D, C, M, int(device)
+        self.summation, self.onehot = "exact", "dense"
         self.set_algo(algo)
 
     def close(self):
@@ -87,6 +88,12 @@ class Plan:
         """"exact" (default) or "avg16" (MADDNESS rounded averaging tree; C % 16 == 0)."""
         _lib.check(self._lib.itlumm_plan_set_summation(self._h, _lib.SUMMATION[summation]))
         self.summation = summation
+
+    def set_onehot(self, onehot: str):
+        """"dense" (default) or "sparse24": the one-hot operand of the tensor-core paths as a
+        compressed 2:4-sparse matrix (tcgen05.mma.sp); bit-identical results."""
+        _lib.check(self._lib.itlumm_plan_set_onehot(self._h, _lib.ONEHOT[onehot]))
+        self.onehot = onehot
 
     @property
     def last_launch_count(self) -> int:

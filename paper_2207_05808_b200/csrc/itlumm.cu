@@ -61,6 +61,8 @@ struct itlumm_plan_s {
   DevPlan dp{};
   SimtCfg simt{};
   TcPlan tc{};
+  TcPlan tcs{};                  // the same tiling with the 2:4-sparse one-hot (f2)
+  itlumm_onehot onehot = ITLUMM_ONEHOT_DENSE;
   // TC_PIPE code scratch (allocated at plan creation; reuse ordered by scratch_ev)
   std::mutex scratch_mu;
   uint8_t* scratch = nullptr;
@@ -259,9 +261,11 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
     for (int h = 0; h < 15; ++h) thr_t[(size_t)h * C + c] = p->thresholds[c * 15 + h];
   std::vector<uint8_t> lut((size_t)C * 16 * Mp, 0);
   for (size_t r = 0; r < (size_t)C * 16; ++r) memcpy(&lut[r * Mp], p->lut + r * M, M);
-  std::vector<uint8_t> qt;
+  std::vector<uint8_t> qt, qs;
   tc_layout_host(C, M, p->lut, &P->tc, qt);
-  const int Mpad = std::max(Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0);   // slice columns past M read 0
+  tc_layout_host(C, M, p->lut, &P->tcs, qs, true);
+  const int Mpad = std::max({Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0,
+                             P->tcs.ok ? P->tcs.G * P->tcs.NS : 0});   // slice columns past M read 0
   std::vector<float> scale(Mpad, 0.f), offtot(Mpad, 0.f), offavg(Mpad, 0.f);
   for (int m = 0; m < M; ++m) {
     scale[m] = p->scale[m];
@@ -276,8 +280,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t o_cols = 0, o_thr = o_cols + al(cols.size() * 4), o_lut = o_thr + al(thr_t.size() * 4),
                o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mpad * 4), o_oa = o_ot + al((size_t)Mpad * 4),
-               o_qt = o_oa + al((size_t)Mpad * 4),
-               total = o_qt + al(qt.size());
+               o_qt = o_oa + al((size_t)Mpad * 4), o_qs = o_qt + al(qt.size()),
+               total = o_qs + al(qs.size());
   int prev = 0;
   cudaGetDevice(&prev);
   auto cleanup = [&](itlumm_status st) {
@@ -299,7 +303,7 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
       {o_cols, cols.data(), cols.size() * 4}, {o_thr, thr_t.data(), thr_t.size() * 4},
       {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mpad * 4},
       {o_ot, offtot.data(), (size_t)Mpad * 4},  {o_oa, offavg.data(), (size_t)Mpad * 4},
-      {o_qt, qt.data(), qt.size()}};
+      {o_qt, qt.data(), qt.size()},           {o_qs, qs.data(), qs.size()}};
   for (auto& c : cp) {
     if (!c.n) continue;
     e = cudaMemcpy(base + c.off, c.src, c.n, cudaMemcpyHostToDevice);
@@ -313,17 +317,20 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   P->dp.offavg = (const float*)(base + o_oa);
   P->dp.D = P->D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
   P->tc.qt = qt.empty() ? nullptr : base + o_qt;
+  P->tcs.qt = qs.empty() ? nullptr : base + o_qs;
   cudaFuncSetAttribute((const void*)k_encode_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   itlumm_status st = configure_simt(P);
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
+  if (st == ITLUMM_OK) st = tc_configure(P->tcs, P->num_sms);
   if (st == ITLUMM_OK && getenv("ITLUMM_TC_TRACE") && atoi(getenv("ITLUMM_TC_TRACE")) != 0) {
     cudaMalloc(&P->tc.trace, ((size_t)16 * 4 * kTraceEv + 4 * 512) * 8);
     if (P->tc.trace) cudaMemset(P->tc.trace, 0, ((size_t)16 * 4 * kTraceEv + 4 * 512) * 8);
+    P->tcs.trace = P->tc.trace;
   }
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
-  if (P->tc.ok) {
+  if (P->tc.ok || P->tcs.ok) {
     P->scratch_ldc = (((C + 1) / 2) + 15) & ~15;
     P->scratch_rows = 262144;
     e = cudaMalloc(&P->scratch, (size_t)P->scratch_rows * P->scratch_ldc);
@@ -388,6 +395,16 @@ extern "C" itlumm_status itlumm_plan_set_summation(itlumm_plan P, itlumm_summati
   if (s == ITLUMM_SUM_AVG16 && P->C % 16 != 0)
     return fail(ITLUMM_EINVAL, "avg16 summation needs C %% 16 == 0 (C = %d)", P->C);
   P->summation = s;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_plan_set_onehot(itlumm_plan P, itlumm_onehot o) {
+  g_err.clear();
+  if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
+  if (o != ITLUMM_ONEHOT_DENSE && o != ITLUMM_ONEHOT_SPARSE24) return fail(ITLUMM_EINVAL, "bad onehot %d", (int)o);
+  if (o == ITLUMM_ONEHOT_SPARSE24 && !P->tcs.ok)
+    return fail(ITLUMM_EUNSUPPORTED, "2:4-sparse one-hot tiling unsupported for this plan: %s", P->tcs.why);
+  P->onehot = o;
   return ITLUMM_OK;
 }
 
@@ -505,17 +522,20 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
   return launch_encode(P, A, dtype, lda, N, codes, ldc, (cudaStream_t)stream);
 }
 
+// The tensor-core tiling in use: dense or 2:4-sparse one-hot.
+static const TcPlan& tcp(itlumm_plan P) { return P->onehot == ITLUMM_ONEHOT_SPARSE24 ? P->tcs : P->tc; }
+
 static bool use_tc(itlumm_plan P) {
   if (P->algo == ITLUMM_ALGO_SIMT || P->summation != ITLUMM_SUM_EXACT) return false;
   if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
-  return tc_preferred(P->tc, P->simt.MS != 0);
+  return tc_preferred(tcp(P), P->simt.MS != 0);
 }
 
 // The fused call runs as encode -> TC accumulate when asked to (TC_PIPE), or under AUTO when
 // the tensor-core tiling splits M over several CTAs (a fused kernel would repeat the gather
 // and the tree walks once per M slice).
 static bool use_pipe(itlumm_plan P) {
-  if (!P->tc.ok || P->summation != ITLUMM_SUM_EXACT) return false;
+  if (!tcp(P).ok || P->summation != ITLUMM_SUM_EXACT) return false;
   if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
   // AUTO pipes every tensor-core shape through the streaming encoder: a streamed LUT has no fused
   // TC kernel, with several slices a fused kernel would repeat the gather per slice, and even with
@@ -528,13 +548,14 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
                                 const uint8_t* codes, int64_t ldc, int64_t N, int32_t* acc, int64_t ldacc,
                                 float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
   if (use_tc(P)) {
-    if (!P->tc.ok) return fail(ITLUMM_EUNSUPPORTED, "tensor-core path unsupported for this plan: %s", P->tc.why);
+    const TcPlan& t = tcp(P);
+    if (!t.ok) return fail(ITLUMM_EUNSUPPORTED, "tensor-core path unsupported for this plan: %s", t.why);
     TcArgs a{};
     a.A = A; a.lda = lda; a.codes = codes; a.ldc = ldc; a.N = N; a.acc = acc; a.ldacc = ldacc;
     a.out = out; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
     bool launched = false;
-    itlumm_status st = fused ? ITLUMM_OK : tc2_launch(P->tc, P->dp, a, s, P->num_sms, false, &launched);
-    if (st == ITLUMM_OK && !launched) st = tc_launch(P->tc, P->dp, fused, dtype == ITLUMM_BF16, a, s);
+    itlumm_status st = (fused || t.sp) ? ITLUMM_OK : tc2_launch(t, P->dp, a, s, P->num_sms, false, &launched);
+    if (st == ITLUMM_OK && !launched) st = tc_launch(t, P->dp, fused, dtype == ITLUMM_BF16, a, s);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     g_launches = 1;
     return ITLUMM_OK;
@@ -590,8 +611,9 @@ static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtyp
     a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;
     a.out = out + (size_t)r0 * ldo; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
     bool launched = false;
-    st = tc2_launch(P->tc, P->dp, a, s, P->num_sms, true, &launched);
-    if (st == ITLUMM_OK && !launched) st = tc_launch(P->tc, P->dp, false, false, a, s, true);
+    const TcPlan& t = tcp(P);
+    if (!t.sp) st = tc2_launch(t, P->dp, a, s, P->num_sms, true, &launched);
+    if (st == ITLUMM_OK && !launched) st = tc_launch(t, P->dp, false, false, a, s, true);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     launches += 2;
   }
@@ -613,6 +635,7 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
   const int enc_warps = kTcThreads / 32 - 1;
   const TcPlan& t = P->tc;
+  if (P->onehot != ITLUMM_ONEHOT_DENSE) return fail(ITLUMM_EUNSUPPORTED, "TC_SP runs the dense one-hot only");
   // split: encoder share ~ bytes read / (bytes read + 1.25 x bytes written) (developer override:
   // ITLUMM_SP_ENC_CTAS)
   static const int enc_override = getenv("ITLUMM_SP_ENC_CTAS") ? atoi(getenv("ITLUMM_SP_ENC_CTAS")) : 0;

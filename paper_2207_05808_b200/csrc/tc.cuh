@@ -41,6 +41,12 @@ constexpr int kTcStages = 3;                                   // default A ring
 constexpr size_t kTcBBudget = 128 * 1024;                      // resident LUT slice budget
 constexpr int kTcStage = 32 * 32 * 4;                          // epilogue staging per warp (bytes)
 constexpr size_t kSmemMax = 227 * 1024;                        // dynamic shared memory per CTA
+// 2:4-sparse one-hot (f2): a one-hot 16-vector has one nonzero per 4 groups of 4, so it is 2:4
+// sparse; stored compressed (2 of every 4 K-elements: 8 B per codebook) with 4 bits of metadata
+// per group, tcgen05.mma.sp doubles K per instruction (K = 64 = 4 codebooks).
+constexpr int kSpA = kTcRows * kKBlock / 2;                    // compressed K-block: 128 rows x 64 B, SWIZZLE_64B
+constexpr int kSpStage = kSpA + kTcRows * 16;                  // + 16 B of metadata per row (tcgen05.cp source)
+constexpr int kSpNsMax = 224;                                  // 2 x NS accumulators + 4 metadata columns per stage <= 512
 
 struct TcPlan {
   bool ok = false;
@@ -49,6 +55,7 @@ struct TcPlan {
   int C = 0, M = 0, KB = 0, NS = 0, G = 0, tmem_cols = 0;
   int CS = 0;                    // codes ring stages (TMA path), 0 = codes path unavailable
   bool stream_b = false;         // LUT too large to stay resident: B K-blocks streamed per stage
+  bool sp = false;               // 2:4-sparse one-hot (tcgen05.mma.sp), NS <= kSpNsMax
   int ST = kTcStages;            // ring stages (one-hot K-blocks, + LUT K-blocks when streamed)
   uint64_t* trace = nullptr;     // developer timeline buffer (ITLUMM_TC_TRACE=1), 8 x 4 x kTraceEv
   size_t smem = 0;
@@ -130,6 +137,38 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// K-major SWIZZLE_64B (8-row atoms of 512 B): the compressed sparse one-hot.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+// Unswizzled 128 rows x 16 B (8-row core groups 128 B apart): the tcgen05.cp metadata source.
+__device__ __forceinline__ uint64_t umma_desc_rows16(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// 2:4-sparse A (bit 2 of the instruction descriptor), metadata at TMEM address e.
+__device__ __forceinline__ void umma_sp_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(tmem_e), "r"(idesc | 4u), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -148,6 +187,50 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t j) {
   return (r >> 3) * 1024u + (r & 7u) * 128u + ((j ^ (r & 7u)) << 4);
 }
 
+// Byte offset of the 16-byte chunk j (0..3) of row r in a K-major SWIZZLE_64B tile.
+__host__ __device__ __forceinline__ uint32_t sw64_off(uint32_t r, uint32_t j) {
+  return (r >> 3) * 512u + (r & 7u) * 64u + ((j ^ ((r >> 1) & 3u)) << 4);
+}
+
+// One row's one-hot K-block (8 codebooks; code 16 = none) into A stage `st`.
+// Dense: 16 B per codebook, byte `code` = 1 (SWIZZLE_128B).  Sparse (2:4): 8 B per codebook, group
+// g = code >> 2 holds the pair of logical positions (e, 3) with values (1, 0) for e = code & 3 < 3,
+// or (0, 3) with values (0, 1) for e = 3; metadata nibble g = idx0 | idx1 << 2, the three empty
+// groups (0, 0) with zero values; the row's 128 metadata bits (codebook j at bits 16j..16j+15)
+// go to the stage's metadata rows.
+template <bool SP>
+__device__ __forceinline__ void put_onehot(uint8_t* st, int r, const uint32_t (&code)[8]) {
+  if (!SP) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t k = code[j];
+      const uint32_t bit = (k < 16) ? (1u << ((k & 3u) * 8u)) : 0u;
+      const uint32_t w = k >> 2;
+      *reinterpret_cast<uint4*>(st + sw128_off(r, j)) =
+          make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
+    }
+  } else {
+    uint32_t meta[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      uint32_t v[2][2], m = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t k = code[2 * jj + h];
+        const uint32_t e = k & 3u, grp = (k >> 2) & 3u;
+        const uint32_t idx = 2u * grp + (e == 3u ? 1u : 0u);     // stored byte of the codebook's 8
+        const uint32_t bit = (k < 16) ? (1u << (8u * (idx & 3u))) : 0u;
+        v[h][0] = idx < 4 ? bit : 0u;
+        v[h][1] = idx < 4 ? 0u : bit;
+        if (k < 16) m |= (0xCu | (e == 3u ? 0u : e)) << (4u * grp + 16u * h);
+      }
+      meta[jj] = m;
+      *reinterpret_cast<uint4*>(st + sw64_off(r, jj)) = make_uint4(v[0][0], v[0][1], v[1][0], v[1][1]);
+    }
+    *reinterpret_cast<uint4*>(st + kSpA + 16 * r) = make_uint4(meta[0], meta[1], meta[2], meta[3]);
+  }
+}
+
 // Shared-memory carve-up (offsets from a 1024-aligned base).
 struct TcSmem {
   size_t b, a, stg, codes, thr, cols, sc, ot, bar, tmem, total;
@@ -156,11 +239,12 @@ struct TcSmem {
 // stream_b: no resident slice; each of the kTcStages stages holds a one-hot K-block and a LUT
 // K-block (NS x 128 B).  fused = false: no threshold/column tables.
 __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS = 0, int ldc_tma = 0,
-                                                 bool stream_b = false, bool fused = true, int ST = kTcStages) {
+                                                 bool stream_b = false, bool fused = true, int ST = kTcStages,
+                                                 bool sp = false) {
   TcSmem s{};
   size_t o = 0;
   s.b = o;    o += stream_b ? (size_t)ST * NS * kKBlock : (size_t)KB * NS * kKBlock;
-  s.a = o;    o += (size_t)ST * kTcRows * kKBlock;
+  s.a = o;    o += (size_t)ST * (sp ? kSpStage : kTcRows * kKBlock);   // both multiples of 1024
   s.stg = o;  o += (size_t)kTcEpiWarps * kTcStage;
   s.codes = o; o += (size_t)CS * kTcRows * ldc_tma;
   if (!fused) C = 0;
@@ -176,7 +260,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
 }
 
 // One persistent CTA of the tensor-core kernel: CTA `cta` of `ncta` (slice = cta % G).
-template <bool FUSED, typename T, bool SB>
+template <bool FUSED, typename T, bool SB, bool SP = false>
 __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const CUtensorMap* out_map,
                                        uint8_t* smem_raw, int cta, int ncta) {
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
@@ -185,7 +269,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   const int CS = FUSED ? 0 : g.CS;
   static_assert(!(FUSED && SB), "the streamed-LUT mode has no fused variant");
   const int ST = g.ST;                                // A (and streamed-B) ring depth
-  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED, ST);
+  const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED, ST, SP);
+  constexpr int kAStage = SP ? kSpStage : kTcRows * kKBlock;
   uint8_t* b_s = smem + L.b;
   uint8_t* codes_s = smem + L.codes;
   uint8_t* a_s = smem + L.a;
@@ -367,17 +452,11 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         const uint8_t* crow = codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
         for (int kb = 0; kb < KB; ++kb) {
           const uint32_t cw = valid ? *reinterpret_cast<const uint32_t*>(crow + kb * 4) : 0u;
-          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
-          uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
+          uint32_t code[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = kb * 8 + j;
-            const uint32_t k = (cw >> (4 * j)) & 15u;
-            const uint32_t bit = (valid && c < C) ? (1u << ((k & 3u) * 8u)) : 0u;
-            const uint32_t w = k >> 2;
-            *reinterpret_cast<uint4*>(st + sw128_off(r, j)) =
-                make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
-          }
+          for (int j = 0; j < 8; ++j) code[j] = (valid && kb * 8 + j < C) ? (cw >> (4 * j)) & 15u : 16u;
+          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
+          put_onehot<SP>(a_s + (size_t)stage * kAStage, r, code);
           fence_proxy_async_smem();
           mbar_arrive(full_bar + stage);
           if (r == 0) stamp(0);
@@ -449,15 +528,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         }
       }
       mbar_wait(empty_bar + stage, phase ^ 1);        // MMA finished reading this stage
-      uint8_t* st = a_s + (size_t)stage * kTcRows * kKBlock;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t k = code[j];
-        const uint32_t bit = (k < 16) ? (1u << ((k & 3u) * 8u)) : 0u;
-        const uint32_t w = k >> 2;
-        const uint4 oh = make_uint4(w == 0 ? bit : 0u, w == 1 ? bit : 0u, w == 2 ? bit : 0u, w == 3 ? bit : 0u);
-        *reinterpret_cast<uint4*>(st + sw128_off(r, j)) = oh;
-      }
+      put_onehot<SP>(a_s + (size_t)stage * kAStage, r, code);
       fence_proxy_async_smem();
       mbar_arrive(full_bar + stage);
       if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -494,12 +565,23 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         mbar_wait(full_bar + stage, phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kTcRows * kKBlock);
+          const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kAStage);
           const uint32_t b_addr = smem_u32(b_s + (size_t)(SB ? stage : kb) * NS * kKBlock);
+          if (SP) {
+            // metadata rows -> TMEM columns 2NS + 4*stage (in tcgen05 issue order before the MMAs
+            // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each)
+            const uint32_t e = tmem_base + (uint32_t)(2 * NS + 4 * stage);
+            tmem_cp_128x128b(e, umma_desc_rows16(a_addr + kSpA));
 #pragma unroll
-          for (int ks = 0; ks < kKBlock / 32; ++ks)
-            umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
-                    (kb | ks) != 0);
+            for (int ks = 0; ks < 2; ++ks)
+              umma_sp_i8(d, umma_desc_sw64(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 64), e + 2 * ks, idesc,
+                         (kb | ks) != 0);
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < kKBlock / 32; ++ks)
+              umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
+                      (kb | ks) != 0);
+          }
           umma_commit(empty_bar + stage);             // frees the A stage when these MMAs finish
           stamp(1);
           if (kb == KB - 1) umma_commit(accf_bar + acc);
@@ -693,10 +775,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   }
 }
 
-template <bool FUSED, typename T, bool SB>
+template <bool FUSED, typename T, bool SB, bool SP = false>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  tc_cta<FUSED, T, SB>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
+  tc_cta<FUSED, T, SB, SP>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -705,9 +787,11 @@ inline const char* tc_last_msg() { return g_tc_msg; }
 
 // Choose the N slice and build the swizzled K-major LUT image: qt[s][kb][n][128 B] with
 // byte (n, k) at sw128_off(n, k/16) + k%16 of block (s, kb); k = 16*(c - 8kb) + code.
-inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vector<uint8_t>& qt) {
+inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vector<uint8_t>& qt, bool sparse = false) {
   qt.clear();
   t->C = C; t->M = M;
+  t->sp = sparse;
+  const int ns_hw = sparse ? kSpNsMax : 256;     // TMEM: 2 accumulators (+ sparse metadata) <= 512 columns
   t->KB = (16 * C + kKBlock - 1) / kKBlock;
   int ns_max = (int)(kTcBBudget / ((size_t)t->KB * kKBlock)) / 32 * 32;
   // N per CTA (<= 256).  Note: a 4-slice split of cfg2 (NS = 128) writes its output
@@ -715,26 +799,28 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   // override (not ABI): ITLUMM_TC_NS_MAX.
   static const int ns_cap = getenv("ITLUMM_TC_NS_MAX") ? atoi(getenv("ITLUMM_TC_NS_MAX")) : 256;
   if (ns_max > ns_cap) ns_max = ns_cap;
-  if (ns_max > 256) ns_max = 256;
+  if (ns_max > ns_hw) ns_max = ns_hw;
   // developer override (not ABI): ITLUMM_TC_STREAM=1 streams the LUT even when it could stay resident
   static const bool force_stream = getenv("ITLUMM_TC_STREAM") && atoi(getenv("ITLUMM_TC_STREAM")) != 0;
   // Stream the LUT when it cannot stay resident, and also when residency would force slices
   // narrower than the 256 columns a streamed slice gets (cfg3 C=64: 57.5 us streamed vs 72.8 us
   // resident with 128-column slices; cfg2 C=32 keeps 256-column resident slices: 24.5 vs 31.8 us).
-  t->stream_b = ns_max < 32 || force_stream || (ns_max < 256 && M > ns_max);
+  t->stream_b = ns_max < 32 || force_stream || (ns_max < ns_hw && M > ns_max);
   if (!t->stream_b) {
     // resident slice only if the fused kernel's full layout fits next to it
     const int G0 = (M + ns_max - 1) / ns_max;
     const int NS0 = ((M + G0 - 1) / G0 + 31) / 32 * 32;
-    if (tc_smem_layout(C, t->KB, NS0, 1, 16 * ((C + 31) / 32), false, true).total > kSmemMax) t->stream_b = true;
+    if (tc_smem_layout(C, t->KB, NS0, 1, 16 * ((C + 31) / 32), false, true, kTcStages, sparse).total > kSmemMax)
+      t->stream_b = true;
   }
-  if (t->stream_b) ns_max = 256;                 // LUT K-blocks streamed per stage (large C)
+  if (t->stream_b) ns_max = ns_hw;               // LUT K-blocks streamed per stage (large C)
   const int G = (M + ns_max - 1) / ns_max;
   int NS = (M + G - 1) / G;
   NS = (NS + 31) / 32 * 32;                      // whole 32-column epilogue chunks
   t->G = G; t->NS = NS;
   int cols = 32;
   while (cols < 2 * NS) cols <<= 1;
+  if (sparse) cols = 512;                        // + 4 metadata columns per ring stage after the accumulators
   t->tmem_cols = cols;
   const size_t blk = (size_t)NS * kKBlock;
   qt.assign((size_t)G * t->KB * blk, 0);
@@ -752,9 +838,9 @@ inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vec
   t->why = "";
 }
 
-template <bool FUSED, typename T, bool SB>
+template <bool FUSED, typename T, bool SB, bool SP = false>
 inline itlumm_status tc_set_attr(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc<FUSED, T, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc<FUSED, T, SB, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
   return ITLUMM_OK;
 }
@@ -766,10 +852,19 @@ inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   static const int st_env = getenv("ITLUMM_TC_STAGES") ? atoi(getenv("ITLUMM_TC_STAGES")) : 0;
   t.ST = kTcStages;
   if (st_env >= 2 && st_env <= 6) t.ST = st_env;
-  else if (tc_smem_layout(t.C, t.KB, t.NS, 1, 16 * ((t.C + 31) / 32), t.stream_b, !t.stream_b, 4).total <= kSmemMax) t.ST = 4;
-  t.smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, t.stream_b, !t.stream_b, t.ST).total;
+  else if (tc_smem_layout(t.C, t.KB, t.NS, 1, 16 * ((t.C + 31) / 32), t.stream_b, !t.stream_b, 4, t.sp).total <= kSmemMax) t.ST = 4;
+  if (t.sp && 2 * t.NS + 4 * t.ST > 512) { t.ok = false; t.why = "TMEM budget exceeded (sparse metadata)"; return ITLUMM_OK; }
+  t.smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, t.stream_b, !t.stream_b, t.ST, t.sp).total;
   if (t.smem > kSmemMax) { t.ok = false; t.why = "shared memory budget exceeded"; return ITLUMM_OK; }
   itlumm_status st;
+  if (t.sp) {
+    if ((st = tc_set_attr<true, float, false, true>(kSmemMax)) != ITLUMM_OK) return st;
+    if ((st = tc_set_attr<true, uint16_t, false, true>(kSmemMax)) != ITLUMM_OK) return st;
+    if ((st = tc_set_attr<false, float, false, true>(kSmemMax)) != ITLUMM_OK) return st;
+    if ((st = tc_set_attr<false, float, true, true>(kSmemMax)) != ITLUMM_OK) return st;
+    t.grid = t.stream_b ? num_sms : t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
+    return ITLUMM_OK;
+  }
   if ((st = tc_set_attr<true, float, false>(kSmemMax)) != ITLUMM_OK) return st;
   if ((st = tc_set_attr<true, uint16_t, false>(kSmemMax)) != ITLUMM_OK) return st;
   if ((st = tc_set_attr<false, float, false>(kSmemMax)) != ITLUMM_OK) return st;
@@ -828,7 +923,7 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
     // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
     for (int cs = 4; cs >= 1; --cs) {
-      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused, t.ST).total;
+      const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused, t.ST, t.sp).total;
       if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { k.CS = cs; smem = need; break; }
     }
   }
@@ -847,7 +942,12 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e;
-  if (fused) {
+  if (t.sp) {
+    if (fused) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false, true>, dp, k, out_map)
+                        : cudaLaunchKernelEx(&cfg, k_tc<true, float, false, true>, dp, k, out_map);
+    else if (t.stream_b) e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true, true>, dp, k, out_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false, true>, dp, k, out_map);
+  } else if (fused) {
     if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false>, dp, k, out_map);
     else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, false>, dp, k, out_map);
   } else if (t.stream_b) {

@@ -5,7 +5,7 @@
 
 int main(void) {
   void* fns[] = {(void*)itlumm_plan_create, (void*)itlumm_plan_destroy, (void*)itlumm_plan_set_algo,
-                 (void*)itlumm_plan_set_summation, (void*)itlumm_plan_info, (void*)itlumm_encode,
+                 (void*)itlumm_plan_set_summation, (void*)itlumm_plan_set_onehot, (void*)itlumm_plan_info, (void*)itlumm_encode,
                  (void*)itlumm_lut_accumulate, (void*)itlumm_amm, (void*)itlumm_amm_host,
                  (void*)itlumm_mlp_create, (void*)itlumm_mlp_destroy, (void*)itlumm_mlp_info,
                  (void*)itlumm_mlp_forward, (void*)itlumm_last_launch_count, (void*)itlumm_last_error,

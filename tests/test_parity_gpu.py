@@ -15,17 +15,23 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = ATOL = 1e-6
-ALGOS = ["simt", "tc", "tc_pipe", "tc_sp"]
+# "_sp24": the same schedule with the 2:4-sparse one-hot operand (tcgen05.mma.sp)
+ALGOS = ["simt", "tc", "tc_pipe", "tc_sp", "tc_sp24", "tc_pipe_sp24"]
+
+
+def _set(plan, algo):
+    if algo.endswith("_sp24"):
+        plan.set_algo(algo[:-5])
+        plan.set_onehot("sparse24")
+    else:
+        plan.set_algo(algo)
+        plan.set_onehot("dense")
 
 
 def _plan(params, algo):
     from paper_2207_05808_b200 import Plan
-    from paper_2207_05808_b200._lib import ItlummError, EUNSUPPORTED
     p = Plan(params, device=0)
-    try:
-        p.set_algo(algo)
-    except ItlummError:
-        raise
+    _set(p, algo)
     return p
 
 
@@ -60,7 +66,7 @@ def run_all(params, A, relu, dtype, algo):
     if params["C"] % 2:
         assert np.all(codes.cpu().numpy()[:, -1] >> 4 == 0)     # R14 padding nibble
     try:
-        plan.set_algo(algo)
+        _set(plan, algo)
         acc = torch.empty((A.shape[0], params["M"]), dtype=torch.int32, device="cuda")
         out, _ = plan.lut_accumulate(codes, acc=acc, relu=relu)
         y = plan.amm(Ad, relu=relu)
@@ -118,7 +124,7 @@ def test_parity_cfg2_full_sampled(algo):
     Ad = _dev(w["A"], "f32")
     codes = plan.encode(Ad)
     try:
-        plan.set_algo(algo)
+        _set(plan, algo)
         y = plan.amm(Ad, relu=True)
         y2, _ = plan.lut_accumulate(codes, relu=True)
     except ItlummError as e:
@@ -153,7 +159,7 @@ def test_edge_strides_alignment_and_specials(algo):
     ref = oracle.amm(params, A, relu=True, want_codes=True)
     plan = _plan(params, "simt")
     try:
-        plan.set_algo(algo)
+        _set(plan, algo)
         Ad = torch.from_numpy(A).cuda()
         big = torch.full((600, 64), -7.0, device="cuda")
         plan.amm(Ad[:, :], out=big[:, :48], relu=True)
