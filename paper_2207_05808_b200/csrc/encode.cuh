@@ -30,6 +30,7 @@ struct EncArgs {
   int row_bytes;        // bytes of one staged row (D * es, multiple of 16)
   int contiguous;       // lda == D: a tile is one bulk copy
   int pdl;              // let a dependent grid launch early (PDL)
+  int a_hint;           // L2 policy of the row reads (l2_policy kind; 0 = default)
   uint64_t* span;       // developer trace: [cta][2] globaltimer at CTA start / end (or null)
 };
 
@@ -79,6 +80,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   if (warp == 0) {
     if (lane == 0) {
       int k = 0;
+      const uint64_t pol = l2_policy(g.a_hint);
       for (int64_t tile = cta; tile < ntiles; tile += ncta, ++k) {
         const int s = k % S;
         if (k >= S) mbar_wait((ready ? pub : empty) + s, (uint32_t)(((k / S) - 1) & 1));
@@ -87,7 +89,8 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
         uint8_t* dst = rows_s + (size_t)s * R * rb;
         mbar_arrive_expect_tx(full + s, (uint32_t)rows * rb);
         if (g.contiguous) {
-          bulk_g2s(dst, A + r0 * ldab, (uint32_t)rows * rb, full + s);
+          if (g.a_hint) bulk_g2s_hint(dst, A + r0 * ldab, (uint32_t)rows * rb, full + s, pol);
+          else bulk_g2s(dst, A + r0 * ldab, (uint32_t)rows * rb, full + s);
         } else {
           for (int r = 0; r < rows; ++r) bulk_g2s(dst + (size_t)r * rb, A + (r0 + r) * ldab, rb, full + s);
         }

@@ -484,6 +484,11 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
       g.R = R; g.S = S; g.row_bytes = (int)rb; g.contiguous = lda == P->D; g.pdl = pdl ? 1 : 0;
+      // Row reads are marked L2 evict_first: streamed once, they should not displace what the step
+      // reuses (cfg2 step 62.9 -> 58.9 us, cfg3 C=64 168.8 -> 158.4 us; profiles/r01/l2_hint_sweep.jsonl).
+      // Developer override: ITLUMM_A_HINT (0 none, 1 evict_first, 2 evict_last, 3/4 evict_first on 1/2 or 1/4).
+      static const int a_hint = getenv("ITLUMM_A_HINT") ? atoi(getenv("ITLUMM_A_HINT")) : 1;
+      g.a_hint = a_hint;
       g.span = P->tc.trace ? P->tc.trace + (size_t)16 * 4 * kTraceEv : nullptr;
       const int64_t ntiles = (N + R - 1) / R;
       const unsigned grid = (unsigned)std::min<int64_t>(ntiles, P->num_sms);

@@ -91,6 +91,7 @@ struct TcKArgs {
   int stream_b;
   int ST;          // ring stages
   int BST;         // k_tc2: LUT-half ring stages
+  int out_hint;    // L2 policy of the output tensor stores (l2_policy kind; 0 = default)
   uint64_t* trace; // developer timeline (ITLUMM_TC_TRACE): [8 CTAs][4 roles][kTraceEv] globaltimer stamps
 };
 constexpr int kTraceEv = 512;
@@ -105,6 +106,10 @@ __device__ __forceinline__ uint64_t gtimer() {
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int x, int y, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -612,6 +617,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       bool pending = false;
       int64_t tile;
       int sl, c0, c1;
+      const uint64_t opol = l2_policy(g.out_hint);
       for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
         mbar_wait(accf_bar + acc, acc_phase);
         tc_fence_after();
@@ -653,7 +659,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(out_map, stg, m0 + j0, row0);
+            if (g.out_hint) tma_store_2d_hint(out_map, stg, m0 + j0, row0, opol);
+            else tma_store_2d(out_map, stg, m0 + j0, row0);
             bulk_commit();
           }
           pending = true;
@@ -914,6 +921,8 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.stream_b = t.stream_b ? 1 : 0;
   k.ST = t.ST;
   k.trace = t.trace;
+  static const int out_hint = getenv("ITLUMM_OUT_HINT") ? atoi(getenv("ITLUMM_OUT_HINT")) : 0;   // developer
+  k.out_hint = out_hint;
   if (t.stream_b && fused) { g_tc_msg = "the LUT is streamed (too large to stay resident): no fused TC kernel"; return ITLUMM_EUNSUPPORTED; }
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
