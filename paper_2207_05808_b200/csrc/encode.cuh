@@ -30,6 +30,7 @@ struct EncArgs {
   int row_bytes;        // bytes of one staged row (D * es, multiple of 16)
   int contiguous;       // lda == D: a tile is one bulk copy
   int pdl;              // let a dependent grid launch early (PDL)
+  int pdl_wait;         // launched as a programmatic dependent: wait for the previous grid before reading A
   int a_hint;           // L2 policy of the row reads (l2_policy kind; 0 = default)
   uint64_t* span;       // developer trace: [cta][2] globaltimer at CTA start / end (or null)
 };
@@ -75,6 +76,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   for (int i = threadIdx.x; i < 15 * C; i += blockDim.x) thr_s[i] = __ldg(p.thr_t + i);
   for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) cols_s[i] = __ldg(p.cols + i);
   __syncthreads();
+  if (g.pdl_wait) pdl_wait();         // A and the codes buffer belong to the stream order
   if (g.pdl) pdl_launch_dependents();
 
   if (warp == 0) {

@@ -471,7 +471,8 @@ static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2,
 // byte length is a multiple of 16) and a 2-stage ring fits in shared memory; otherwise the
 // per-thread gather kernel k_encode.
 static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda,
-                                   int64_t N, uint8_t* codes, int64_t ldc, cudaStream_t s, bool pdl = false) {
+                                   int64_t N, uint8_t* codes, int64_t ldc, cudaStream_t s, bool pdl = false,
+                                   bool pdl_dep = false) {
   const int es = dtype == ITLUMM_BF16 ? 2 : 4;
   const int64_t rb = (int64_t)P->D * es;
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
@@ -493,10 +494,27 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       const int64_t ntiles = (N + R - 1) / R;
       const unsigned grid = (unsigned)std::min<int64_t>(ntiles, P->num_sms);
       const size_t smem = enc_smem_bytes(P->C, R, S, (int)rb);
+      // pdl_dep: a programmatic dependent of the previous kernel on the stream (the prologue
+      // overlaps its tail; griddepcontrol.wait before any read of A).  Only for single-wave
+      // encodes, which are launch-latency bound (cfg1: 7.67 -> 6.35 us per call); multi-wave ones
+      // got slower (cfg2 58.8 -> 63.6 us; profiles/r01/encoder_pdl.jsonl).  Developer override:
+      // ITLUMM_ENC_PDL (0 never, 1 single-wave, 2 always).
+      static const int dep_env = getenv("ITLUMM_ENC_PDL") ? atoi(getenv("ITLUMM_ENC_PDL")) : 1;
+      g.pdl_wait = (pdl_dep && (dep_env == 2 || (dep_env == 1 && ntiles <= P->num_sms))) ? 1 : 0;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kEncThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = g.pdl_wait ? 1 : 0;
       if (dtype == ITLUMM_F32)
-        k_encode_rows<float><<<grid, kEncThreads, smem, s>>>(P->dp, g);
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_encode_rows<float>, P->dp, g));
       else
-        k_encode_rows<uint16_t><<<grid, kEncThreads, smem, s>>>(P->dp, g);
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_encode_rows<uint16_t>, P->dp, g));
       CUDA_TRY(cudaGetLastError());
       g_launches = 1;
       return ITLUMM_OK;
@@ -610,7 +628,7 @@ static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtyp
   for (int64_t r0 = 0; r0 < N; r0 += P->scratch_rows) {
     const int64_t rows = std::min<int64_t>(P->scratch_rows, N - r0);
     const void* Ar = (const uint8_t*)A + (size_t)r0 * lda * es;
-    itlumm_status st = launch_encode(P, Ar, dtype, lda, rows, P->scratch, P->scratch_ldc, s, true);
+    itlumm_status st = launch_encode(P, Ar, dtype, lda, rows, P->scratch, P->scratch_ldc, s, true, true);
     if (st != ITLUMM_OK) return st;
     TcArgs a{};
     a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;

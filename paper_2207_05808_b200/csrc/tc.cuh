@@ -391,6 +391,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   // Everything above touched only plan memory; the codes (and `out`) belong to the stream
   // order, so a programmatic dependent waits here for the encode grid to complete.
   if (g.pdl) pdl_wait();
+  pdl_launch_dependents();           // a programmatically dependent next encoder may start its prologue
 
   if (warp == kTcLoaderWarp) {
     // ============================================================== codes loader (one lane)
