@@ -51,7 +51,10 @@ __host__ __device__ inline size_t enc_smem_bytes(int C, int R, int S, int row_by
 // One persistent encoder CTA (`cta` of `ncta`) with warp 0 as the bulk-copy producer and
 // blockDim/32 - 1 consumer warps.  ready != nullptr (spatial pipeline): once every consumer warp
 // is done with an encode tile, the producer thread adds 1 to ready[row0 / 128].
-template <typename T>
+// WIDE (C >= 32): a warp unit is one 32-codebook group of one row, units taken in turn; the
+// general (row, codebook) lane mapping below is compiled out (it measured slower for C = 256:
+// cfg4 layer-1 encode 685 -> 783 us, when both lived in one kernel).
+template <typename T, bool WIDE>
 __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint8_t* smem, int cta, int ncta,
                                         uint32_t* ready) {
   const int nconsumer = (int)(blockDim.x >> 5) - (ready ? 2 : 1);   // warp 1 publishes when ready
@@ -147,7 +150,25 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
     const int64_t r0 = tile * R;
     const int nrows = (int)((g.N - r0) < R ? (g.N - r0) : R);
     const int nunits = ((nrows + rpu - 1) / rpu) * ngrp;
-    if (nunits <= nconsumer) {                         // at most one unit per warp (cfg2 shapes)
+    if (WIDE) {
+      for (int u = cw; u < nrows * ngrp; u += nconsumer) {
+        const int r = u / ngrp, grp = u - r * ngrp;
+        const int c = grp * 32 + lane;
+        uint32_t code = 0;
+        if (c < C) {
+          const T* a = rows + (size_t)r * rs;
+          const int4 col = *reinterpret_cast<const int4*>(cols_s + 4 * c);
+          float v[4];
+          v[0] = InTraits<T>::lds(a + col.x);
+          v[1] = InTraits<T>::lds(a + col.y);
+          v[2] = InTraits<T>::lds(a + col.z);
+          v[3] = InTraits<T>::lds(a + col.w);
+          code = (uint32_t)tree_walk(v, thr_s, C, c);
+        }
+        const uint32_t hi = __shfl_down_sync(0xffffffffu, code, 1);
+        if (!(lane & 1) && c < C) g.codes[(r0 + r) * g.ldc + (c >> 1)] = (uint8_t)(code | (hi << 4));
+      }
+    } else if (nunits <= nconsumer) {                         // at most one unit per warp (cfg2 shapes)
       if (cw < nunits) {
         const int ur = cw / ngrp, grp = cw - ur * ngrp;
         const int r = ur * rpu + rsub, c = grp * 32 + cl;
@@ -166,7 +187,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
         if (!(lane & 1) && r < nrows && c < C) g.codes[(r0 + r) * g.ldc + (c >> 1)] = (uint8_t)(code | (hi << 4));
       }
     } else
-    // two units per pass: their shared-memory gathers and tree walks overlap
+    // short rows (C < 32): two units per pass, their shared-memory gathers and tree walks overlap
     for (int u0 = cw; u0 < nunits; u0 += 2 * nconsumer) {
       uint32_t code[2];
       int rr[2], cc[2];
@@ -202,10 +223,10 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   if (g.span && cw == 0 && lane == 0) g.span[2 * cta + 1] = gtimer_ns();
 }
 
-template <typename T>
+template <typename T, bool WIDE>
 __global__ void __launch_bounds__(kEncThreads, 1) k_encode_rows(DevPlan p, EncArgs g) {
   extern __shared__ __align__(16) uint8_t smem_enc[];
-  enc_cta<T>(p, g, smem_enc, blockIdx.x, gridDim.x, nullptr);
+  enc_cta<T, WIDE>(p, g, smem_enc, blockIdx.x, gridDim.x, nullptr);
 }
 
 }  // namespace itlumm

@@ -318,8 +318,10 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   P->dp.D = P->D; P->dp.C = C; P->dp.M = M; P->dp.Mp = Mp;
   P->tc.qt = qt.empty() ? nullptr : base + o_qt;
   P->tcs.qt = qs.empty() ? nullptr : base + o_qs;
-  cudaFuncSetAttribute((const void*)k_encode_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute((const void*)k_encode_rows<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute((const void*)k_encode_rows<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute((const void*)k_encode_rows<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   itlumm_status st = configure_simt(P);
   if (st != ITLUMM_OK) return cleanup(st);
   st = tc_configure(P->tc, P->num_sms);
@@ -511,10 +513,11 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = g.pdl_wait ? 1 : 0;
+      const bool wide = P->C >= 32;
       if (dtype == ITLUMM_F32)
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_encode_rows<float>, P->dp, g));
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, wide ? k_encode_rows<float, true> : k_encode_rows<float, false>, P->dp, g));
       else
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, k_encode_rows<uint16_t>, P->dp, g));
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, wide ? k_encode_rows<uint16_t, true> : k_encode_rows<uint16_t, false>, P->dp, g));
       CUDA_TRY(cudaGetLastError());
       g_launches = 1;
       return ITLUMM_OK;

@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_amm_sp(DevPlan p, EncArgs ge,
                                                          const __grid_constant__ CUtensorMap out_map) {
   extern __shared__ __align__(1024) uint8_t smem_sp[];
   if ((int)blockIdx.x < sp.E) {
-    enc_cta<T>(p, ge, smem_sp, blockIdx.x, sp.E, gt.ready);
+    if (p.C >= 32) enc_cta<T, true>(p, ge, smem_sp, blockIdx.x, sp.E, gt.ready);
+    else enc_cta<T, false>(p, ge, smem_sp, blockIdx.x, sp.E, gt.ready);
   } else {
     tc_cta<false, float, SB>(p, gt, &out_map, smem_sp, blockIdx.x - sp.E, gridDim.x - sp.E);
   }
