@@ -554,48 +554,52 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     }
   } else if (warp == kTcMmaWarp) {
     // ============================================================== MMA issuer
-    const uint32_t idesc = idesc_i8(NS);
-    if (!SB) mbar_wait(b_bar, 0);                    // resident LUT slice in shared memory
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int64_t tile;
-    int sl;
-    for (int64_t k = 0; item(k, tile, sl); ++k) {
-      mbar_wait(acce_bar + acc, acc_phase ^ 1);      // epilogue drained this accumulator
-      if (lane == 0) stamp(1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + (uint32_t)(acc * NS);
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(full_bar + stage, phase);
+    // One thread, kept lean: the tensor core only stays busy if the issuing thread turns a K-block
+    // around in less than its MMA time (272 ns at N=256); descriptors are precomputed and advanced
+    // by adding to the start-address field (addr >> 4; shared addresses < 256 KB never carry).
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8(NS);
+      if (!SB) mbar_wait(b_bar, 0);                  // resident LUT slice in shared memory
+      const uint32_t a0 = smem_u32(a_s);
+      const uint64_t a_desc0 = SP ? umma_desc_sw64(a0) : umma_desc_sw128(a0);
+      const uint64_t m_desc0 = umma_desc_rows16(a0 + kSpA);
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(b_s));
+      const uint32_t a_step = (uint32_t)kAStage >> 4, b_step = (uint32_t)(NS * kKBlock) >> 4;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k) {
+        mbar_wait(acce_bar + acc, acc_phase ^ 1);    // epilogue drained this accumulator
+        stamp(1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(a_s + (size_t)stage * kAStage);
-          const uint32_t b_addr = smem_u32(b_s + (size_t)(SB ? stage : kb) * NS * kKBlock);
+        const uint32_t d = tmem_base + (uint32_t)(acc * NS);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(full_bar + stage, phase);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
+          const uint64_t bd = b_desc0 + (uint64_t)((SB ? stage : kb) * b_step);
           if (SP) {
             // metadata rows -> TMEM columns 2NS + 4*stage (in tcgen05 issue order before the MMAs
-            // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each)
+            // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each; A +32 B, B +64 B)
             const uint32_t e = tmem_base + (uint32_t)(2 * NS + 4 * stage);
-            tmem_cp_128x128b(e, umma_desc_rows16(a_addr + kSpA));
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-              umma_sp_i8(d, umma_desc_sw64(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 64), e + 2 * ks, idesc,
-                         (kb | ks) != 0);
+            tmem_cp_128x128b(e, m_desc0 + (uint64_t)(stage * a_step));
+            umma_sp_i8(d, ad, bd, e, idesc, kb != 0);
+            umma_sp_i8(d, ad + 2, bd + 4, e + 2, idesc, 1u);
           } else {
-#pragma unroll
-            for (int ks = 0; ks < kKBlock / 32; ++ks)
-              umma_i8(d, umma_desc_sw128(a_addr + ks * 32), umma_desc_sw128(b_addr + ks * 32), idesc,
-                      (kb | ks) != 0);
+            umma_i8(d, ad, bd, idesc, kb != 0);          // K = 32 per MMA: +32 B on both operands
+            umma_i8(d, ad + 2, bd + 2, idesc, 1u);
+            umma_i8(d, ad + 4, bd + 4, idesc, 1u);
+            umma_i8(d, ad + 6, bd + 6, idesc, 1u);
           }
-          umma_commit(empty_bar + stage);             // frees the A stage when these MMAs finish
-          stamp(1);
+          umma_commit(empty_bar + stage);             // frees the stage when these MMAs finish
           if (kb == KB - 1) umma_commit(accf_bar + acc);
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == ST) { stage = 0; phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ============================================================== epilogue
