@@ -34,10 +34,38 @@ WORKLOAD_DESC = {
     "cfg3_c128": "BASELINE configs[2]: CIFAR-shaped layer, N=50000 D=3072 M=1024 C=128",
     "cfg5": "BASELINE configs[4]: FFN-shaped stress case, N=262144 D=4096 M=4096 C=256, bf16 input",
 }
+for _w in ("cfg2", "cfg3_c64", "cfg3_c128", "cfg5"):
+    WORKLOAD_DESC[_w + "_packed"] = (WORKLOAD_DESC[_w] + "; SPLIT-PACKED input: each row holds only its 4C split "
+                                     "values in [c][level] order (the same layer re-parameterised, bit-identical "
+                                     "outputs; SURVEY 8(d) judges the 70% HBM target on this layout)")
 for _c in synth.MLP_CFG["C_sweep"]:
     WORKLOAD_DESC[f"cfg4_c{_c}"] = (f"BASELINE configs[3]: whole 3-layer ReLU MLP 3072-1024-1024-10, every layer "
                                    f"ITLUMM with C={_c}, N=1048576 CIFAR-shaped rows (itlumm_mlp_forward)")
 METRIC = "fused ITLUMM rows/s"
+
+
+def base_workload(workload: str):
+    """(base config name, split-packed?) of a workload name."""
+    return (workload[:-7], True) if workload.endswith("_packed") else (workload, False)
+
+
+def _split_packed(params: dict):
+    """Bench-local split-packed re-parameterisation (host indexing only, shared by both arms; the
+    product exposes the same as paper_2207_05808_b200.split_packed): cols[c][t] =
+    perm[b_c + split_dim[c][t]]; the packed layer has D = 4C, identity perm, 4-dim chunks."""
+    D, C = int(params["D"]), int(params["C"])
+    perm = np.arange(D) if params.get("perm") is None else np.asarray(params["perm"], np.int64)
+    if params.get("boundaries") is None:
+        sizes = np.full(C, D // C)
+        sizes[: D % C] += 1
+        bnd = np.concatenate([[0], np.cumsum(sizes)])
+    else:
+        bnd = np.asarray(params["boundaries"], np.int64)
+    cols = perm[bnd[:C, None] + np.asarray(params["split_dim"], np.int64).reshape(C, 4)].reshape(-1)
+    packed = {k: v for k, v in params.items() if k != "T"}
+    packed.update(D=4 * C, perm=np.arange(4 * C, dtype=np.int32), boundaries=np.arange(0, 4 * C + 1, 4, dtype=np.int32),
+                  split_dim=np.tile(np.arange(4, dtype=np.int32), (C, 1)))
+    return packed, cols
 
 
 def _rows_chunk(a):
@@ -148,7 +176,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = synth.CONFIGS[args.workload]
+    base, packed = base_workload(args.workload)
+    cfg = synth.CONFIGS[base]
     n = cfg["N"] if args.rows is None else args.rows
     relu = cfg["relu"]
     bf16 = cfg["dtype"] == "bf16"
@@ -156,18 +185,25 @@ def run_ours(args):
     # offline fit on rank 0 (host), broadcast once over NCCL, plan on every rank
     params = None
     if rank == 0:
-        w0 = synth.workload(args.workload, n_rows=0)
+        w0 = synth.workload(base, n_rows=0)
         params = fit_layer(w0["A_train"], w0["B"], w0["C"], w0["perm"], w0["bias"], a_is_bf16=bf16)
     if world > 1:
         params = pdist.broadcast_params(params, dev)
+    cols = None
+    if packed:
+        params, cols = _split_packed(params)
     plan = Plan(params, device=local, algo=args.algo)
 
     # this rank's rows (weak scaling: rank r owns rows [r*n, (r+1)*n) of the seeded stream)
     r0, r1 = pdist.weak_rows(n, rank)
     A_host = synth.rows(cfg["dist"], cfg["cfg"], 0, r0, r1, cfg["D"])
+    if packed:
+        A_host = np.ascontiguousarray(A_host[:, cols])
     A_t = torch.from_numpy(A_host.view(np.int16) if bf16 else A_host)
     A_pin = A_t.pin_memory()
-    nbuf = 2
+    # rotate enough A/out buffer sets that the inputs read between two uses of a buffer exceed
+    # twice the L2 (126 MB): 2 sets for row-major inputs, more for split-packed ones
+    nbuf = int(min(16, max(2, -(-(256 << 20) // max(1, A_host.nbytes)))))
     A_dev = [A_pin.to(dev) for _ in range(nbuf)]
     if bf16:
         A_dev = [a.view(torch.bfloat16) for a in A_dev]
@@ -245,7 +281,8 @@ def run_ours(args):
         kernels = [
             {"kernel": "k_encode_rows (a1+a2)", "ms": t_enc, "alg_bytes": b_enc,
              "achieved_GBps": b_enc / (t_enc * 1e-3) / 1e9,
-             "note": "reads whole rows: the 4C split columns touch ~every DRAM line of a row"},
+             "note": ("split-packed rows: 4C values per row, contiguous" if packed else
+                      "reads whole rows: the 4C split columns touch ~every DRAM line of a row")},
             {"kernel": "k_tc (a3' one-hot x LUT on tcgen05 + a4)", "ms": t_acc, "alg_bytes": b_acc,
              "achieved_GBps": b_acc / (t_acc * 1e-3) / 1e9},
         ]
@@ -278,19 +315,19 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(args.workload, params, n, budget_s=args.cpu_budget)
+            cpu = cpu_baseline(args.workload, params, n, budget_s=args.cpu_budget, cols=cols)
         line = {
             "metric": METRIC, "value": rows_per_s, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded stand-in for the dataset, DESIGN.md input recipe)",
             "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
-                       "rows_per_gpu": n, "global_rows": n * world, "D": cfg["D"], "C": cfg["C"],
-                       "M": cfg["M"], "input": ("bf16" if bf16 else "f32") + " row-major",
+                       "rows_per_gpu": n, "global_rows": n * world, "D": int(params["D"]), "C": cfg["C"],
+                       "M": cfg["M"], "input": ("bf16" if bf16 else "f32") + (" split-packed" if packed else " row-major"),
                        "epilogue": "relu" if relu else "none", "algo": args.algo,
                        "parallelism": f"rows sharded dp{world}",
-                       "l2": f"inputs larger than L2 (A {A_host.nbytes / 2**20:.0f} MiB/step) and "
-                             f"{nbuf} rotating A/out buffer sets",
+                       "l2": f"inputs larger than L2: A {A_host.nbytes / 2**20:.0f} MiB per step, {nbuf} rotating "
+                             f"A/out buffer sets ({nbuf * A_host.nbytes / 2**20:.0f} MiB of A between reuses of a buffer)",
                        "timing": "K steps captured as one CUDA graph, replayed once between CUDA events",
                        "compute": "uint8 LUT, exact int32 accumulate, fp32 compare + fmaf dequant"},
             "output_elems_per_s": rows_per_s * cfg["M"],
@@ -451,16 +488,17 @@ def _oracle_rows_per_s(params, A, relu, dtype, nthreads):
     return A.shape[0] / (time.perf_counter() - t0)
 
 
-def cpu_baseline(workload: str, params: dict, n: int, budget_s: float = 15.0):
+def cpu_baseline(workload: str, params: dict, n: int, budget_s: float = 15.0, cols=None):
     """The oracle (plain C, never tuned) on the host cores, on a bounded sample of the same
     workload (fitted parameters shared); ~budget_s seconds of work."""
-    cfg = synth.CONFIGS[workload]
+    cfg = synth.CONFIGS[base_workload(workload)[0]]
     cores = os.cpu_count() or 1
     dtype = "bf16" if cfg["dtype"] == "bf16" else "f32"
-    probe = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"])
+    sel = (lambda a: np.ascontiguousarray(a[:, cols])) if cols is not None else (lambda a: a)
+    probe = sel(synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"]))
     rate = _oracle_rows_per_s(params, probe, cfg["relu"], dtype, cores)
     n_s = int(max(512, min(n, rate * budget_s)))
-    A = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, n_s, cfg["D"])
+    A = sel(synth.rows(cfg["dist"], cfg["cfg"], 0, 0, n_s, cfg["D"]))
     v = _oracle_rows_per_s(params, A, cfg["relu"], dtype, cores)
     return {"value": v, "unit": "rows/s", "cores": cores, "kind": "oracle",
             "sample": f"first {n_s} of the {n} rows of {workload} (rank 0), full encode+accumulate+dequant"}
@@ -475,17 +513,22 @@ def run_reference(args):
     from oracle import fit as ofit
     if args.workload.startswith("cfg4"):
         return run_reference_mlp(args)
-    cfg = synth.CONFIGS[args.workload]
+    base, packed = base_workload(args.workload)
+    cfg = synth.CONFIGS[base]
     n = cfg["N"] if args.rows is None else args.rows
-    w0 = synth.workload(args.workload, n_rows=0)
+    w0 = synth.workload(base, n_rows=0)
     bf16 = cfg["dtype"] == "bf16"
     params = ofit.fit(w0["A_train"], w0["B"], w0["C"], w0["perm"], w0["bias"], a_is_bf16=bf16)
+    cols = None
+    if packed:
+        params, cols = _split_packed(params)
+    sel = (lambda a: np.ascontiguousarray(a[:, cols])) if packed else (lambda a: a)
     dtype = "bf16" if bf16 else "f32"
     cores = os.cpu_count() or 1
-    probe = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"])
+    probe = sel(synth.rows(cfg["dist"], cfg["cfg"], 0, 0, min(n, 512), cfg["D"]))
     rate = _oracle_rows_per_s(params, probe, cfg["relu"], dtype, cores)
     per_step = int(max(1, min(n, rate * args.ref_budget / max(1, args.steps + args.warmup))))
-    A = synth.rows(cfg["dist"], cfg["cfg"], 0, 0, per_step, cfg["D"])
+    A = sel(synth.rows(cfg["dist"], cfg["cfg"], 0, 0, per_step, cfg["D"]))
     for _ in range(args.warmup):
         oracle.amm(params, A, relu=cfg["relu"], dtype=dtype, nthreads=cores)
     t0 = time.perf_counter()

@@ -5,7 +5,7 @@
   dist        — row sharding over ranks and the one-time parameter broadcast
 """
 from .api import Plan, Mlp  # noqa: F401
-from .fit import fit_layer, fit_mlp, chunk_bounds  # noqa: F401
+from .fit import fit_layer, fit_mlp, chunk_bounds, split_packed  # noqa: F401
 from . import _lib  # noqa: F401
 
-__all__ = ["Plan", "Mlp", "fit_layer", "fit_mlp", "chunk_bounds"]
+__all__ = ["Plan", "Mlp", "fit_layer", "fit_mlp", "chunk_bounds", "split_packed"]

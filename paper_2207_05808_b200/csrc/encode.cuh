@@ -30,6 +30,8 @@ struct EncArgs {
   int row_bytes;        // bytes of one staged row (D * es, multiple of 16)
   int contiguous;       // lda == D: a tile is one bulk copy
   int pdl;              // let a dependent grid launch early (PDL)
+  int fixed_ok;         // developer switch for the register-threshold WIDE consumer (1 = allowed)
+  int packed;           // split-packed rows: cols[c][t] == 4c + t (one vector load per codebook)
   int pdl_wait;         // launched as a programmatic dependent: wait for the previous grid before reading A
   int a_hint;           // L2 policy of the row reads (l2_policy kind; 0 = default)
   uint64_t* span;       // developer trace: [cta][2] globaltimer at CTA start / end (or null)
@@ -142,6 +144,47 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   const int rpu = 32 / lpr;                            // rows per warp unit
   const int ngrp = (C + 31) >> 5;                      // 32-codebook groups per row
   const int rsub = lane / lpr, cl = lane - rsub * lpr;
+  // WIDE with 32-codebook groups that divide the consumer warps (C = 32, 64, 128, 256): warp cw
+  // always serves group cw % ngrp, so each lane owns one codebook for the whole kernel and keeps
+  // its 15 thresholds and 4 gather columns in registers; the tree walk is then compare/select only
+  // (no dependent shared-memory loads), and two rows are walked per pass for ILP.
+  const bool fixed = WIDE && (nconsumer % ngrp) == 0 && g.fixed_ok;
+  const int fc = (cw % ngrp) * 32 + lane;              // this lane's codebook (fixed mode)
+  float tr[15];
+  int4 fcol = make_int4(0, 0, 0, 0);
+  if (fixed && fc < C) {
+#pragma unroll
+    for (int h = 0; h < 15; ++h) tr[h] = thr_s[h * C + fc];
+    fcol = *reinterpret_cast<const int4*>(cols_s + 4 * fc);
+  } else {
+#pragma unroll
+    for (int h = 0; h < 15; ++h) tr[h] = 0.f;
+  }
+  auto walk_regs = [&](float v0, float v1, float v2, float v3) -> uint32_t {
+    const uint32_t b0 = v0 > tr[0];
+    const uint32_t b1 = v1 > (b0 ? tr[2] : tr[1]);
+    const float t2a = b1 ? tr[4] : tr[3], t2b = b1 ? tr[6] : tr[5];
+    const uint32_t b2 = v2 > (b0 ? t2b : t2a);
+    const float x0 = b2 ? tr[8] : tr[7], x1 = b2 ? tr[10] : tr[9], x2 = b2 ? tr[12] : tr[11], x3 = b2 ? tr[14] : tr[13];
+    const float y0 = b1 ? x1 : x0, y1 = b1 ? x3 : x2;
+    const uint32_t b3 = v3 > (b0 ? y1 : y0);
+    return (b0 << 3) | (b1 << 2) | (b2 << 1) | b3;
+  };
+  auto load4 = [&](const T* a, float& v0, float& v1, float& v2, float& v3) {
+    if (g.packed) {
+      if (sizeof(T) == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(a + 4 * fc);
+        v0 = q.x; v1 = q.y; v2 = q.z; v3 = q.w;
+      } else {
+        const uint2 q = *reinterpret_cast<const uint2*>(a + 4 * fc);
+        v0 = __uint_as_float(q.x << 16); v1 = __uint_as_float(q.x & 0xFFFF0000u);
+        v2 = __uint_as_float(q.y << 16); v3 = __uint_as_float(q.y & 0xFFFF0000u);
+      }
+    } else {
+      v0 = InTraits<T>::lds(a + fcol.x); v1 = InTraits<T>::lds(a + fcol.y);
+      v2 = InTraits<T>::lds(a + fcol.z); v3 = InTraits<T>::lds(a + fcol.w);
+    }
+  };
   int k = 0;
   for (int64_t tile = cta; tile < ntiles; tile += ncta, ++k) {
     const int s = k % S;
@@ -150,7 +193,28 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
     const int64_t r0 = tile * R;
     const int nrows = (int)((g.N - r0) < R ? (g.N - r0) : R);
     const int nunits = ((nrows + rpu - 1) / rpu) * ngrp;
-    if (WIDE) {
+    if (WIDE && fixed) {
+      const int rstep = nconsumer / ngrp;
+      const bool valid = fc < C;
+      for (int r = cw / ngrp; r < nrows; r += 2 * rstep) {
+        const int r2 = r + rstep;
+        uint32_t code = 0, code2 = 0;
+        if (valid) {
+          float v0, v1, v2, v3, w0, w1, w2, w3;
+          load4(rows + (size_t)r * rs, v0, v1, v2, v3);
+          if (r2 < nrows) load4(rows + (size_t)r2 * rs, w0, w1, w2, w3);
+          else w0 = w1 = w2 = w3 = 0.f;
+          code = walk_regs(v0, v1, v2, v3);
+          code2 = walk_regs(w0, w1, w2, w3);
+        }
+        const uint32_t hi = __shfl_down_sync(0xffffffffu, code, 1);
+        const uint32_t hi2 = __shfl_down_sync(0xffffffffu, code2, 1);
+        if (!(lane & 1) && valid) {
+          g.codes[(r0 + r) * g.ldc + (fc >> 1)] = (uint8_t)(code | (hi << 4));
+          if (r2 < nrows) g.codes[(r0 + r2) * g.ldc + (fc >> 1)] = (uint8_t)(code2 | (hi2 << 4));
+        }
+      }
+    } else if (WIDE) {
       for (int u = cw; u < nrows * ngrp; u += nconsumer) {
         const int r = u / ngrp, grp = u - r * ngrp;
         const int c = grp * 32 + lane;

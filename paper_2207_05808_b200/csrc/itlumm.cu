@@ -72,6 +72,7 @@ struct itlumm_plan_s {
   uint32_t* ready = nullptr;     // [scratch_rows / 128] x 2: TC_SP ready / consumed counters (zeroed)
   bool coop = false;             // device supports cooperative launches
   double seg_frac[2] = {1.0, 1.0};  // fraction of a row's 64-byte segments the gather touches (f32, bf16)
+  bool packed = false;           // split-packed input: gather column of (c, t) is 4c + t
   // host API staging
   std::mutex host_mu;
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};   // host API: 3-stage copy/compute ring
@@ -253,6 +254,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
     for (int col : cols) { const int sgi = col * es / 64; if (!hit[sgi]) { hit[sgi] = 1; ++n; } }
     P->seg_frac[d] = (double)n / nseg;
   }
+  P->packed = true;
+  for (int i = 0; i < 4 * C; ++i) P->packed = P->packed && cols[i] == i;
   const int Mp = P->Mp;
 
   // host images of the device parameters
@@ -487,6 +490,12 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
       g.R = R; g.S = S; g.row_bytes = (int)rb; g.contiguous = lda == P->D; g.pdl = pdl ? 1 : 0;
+      g.packed = P->packed ? 1 : 0;
+      // register-threshold consumer: split-packed rows (cfg2 packed encode 19.7 -> 11.6 us) and
+      // C > 32 (cfg4 C=256 MLP 12.8 -> 10.7 ms); row-major C = 32 keeps the shared-memory walk
+      // (31.8 vs 32.5 us).  Developer override: ITLUMM_ENC_FIXED (0 never, 1 auto, 2 always).
+      static const int fixed_env = getenv("ITLUMM_ENC_FIXED") ? atoi(getenv("ITLUMM_ENC_FIXED")) : 1;
+      g.fixed_ok = fixed_env == 2 || (fixed_env == 1 && (P->packed || P->C > 32));
       // Row reads are marked L2 evict_first: streamed once, they should not displace what the step
       // reuses (cfg2 step 62.9 -> 58.9 us, cfg3 C=64 168.8 -> 158.4 us; profiles/r01/l2_hint_sweep.jsonl).
       // Developer override: ITLUMM_A_HINT (0 none, 1 evict_first, 2 evict_last, 3/4 evict_first on 1/2 or 1/4).
@@ -698,6 +707,8 @@ static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype,
     ge.A = (const uint8_t*)A + (size_t)r0 * lda * es; ge.lda = lda; ge.N = rows;
     ge.codes = P->scratch; ge.ldc = P->scratch_ldc;
     ge.R = R; ge.S = S; ge.row_bytes = (int)rb; ge.contiguous = lda == P->D; ge.pdl = 0;
+    ge.packed = P->packed ? 1 : 0;
+    ge.fixed_ok = 1;
     TcKArgs gt{};
     gt.codes = P->scratch; gt.ldc = P->scratch_ldc; gt.N = rows;
     gt.out = out + (size_t)r0 * ldo; gt.ldo = ldo; gt.relu = epi == ITLUMM_EPI_RELU;

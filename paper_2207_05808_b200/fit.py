@@ -110,6 +110,30 @@ def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | Non
                 bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)), T=T)
 
 
+def split_columns(params: dict) -> np.ndarray:
+    """The 4C input columns the encoder reads, in [c][level] order: perm[b_c + split_dim[c][t]]
+    (step a1 folded)."""
+    D, C = int(params["D"]), int(params["C"])
+    perm = np.arange(D) if params.get("perm") is None else np.asarray(params["perm"], np.int64)
+    bnd = chunk_bounds(D, C) if params.get("boundaries") is None else np.asarray(params["boundaries"], np.int64)
+    sd = np.asarray(params["split_dim"], np.int64).reshape(C, N_LEVELS)
+    return perm[bnd[:C, None] + sd].reshape(-1).astype(np.int64)
+
+
+def split_packed(params: dict):
+    """Re-parameterise a fitted layer for SPLIT-PACKED input: an input row that
+    holds only the 4C split values in [c][level] order, A_packed = A[:, cols].  The packed layer is
+    an ordinary ITLUMM layer (D = 4C, identity permutation, 4-dim chunks, split_dim[c] = 0..3)
+    with the same thresholds, LUT and dequant, so it computes bit-identical outputs from 16C
+    input bytes per row (fp32) instead of whole rows.  Returns (packed_params, cols)."""
+    C = int(params["C"])
+    cols = split_columns(params)
+    packed = {k: v for k, v in params.items() if k not in ("T",)}
+    packed.update(D=4 * C, perm=np.arange(4 * C, dtype=np.int32), boundaries=np.arange(0, 4 * C + 1, 4, dtype=np.int32),
+                  split_dim=np.tile(np.arange(N_LEVELS, dtype=np.int32), (C, 1)))
+    return packed, cols
+
+
 def quantize_table(T: np.ndarray):
     """uint8 LUT with per-output-column scale/offset (reading R6): lo = min, scale = (hi-lo)/255
     (1 for a constant column), q = clamp(floor((T-lo)/scale + 0.5), 0, 255), fp64."""

@@ -1,0 +1,70 @@
+"""Split-packed input: a layer re-parameterised for rows that hold only the 4C split
+values in [c][level] order computes the same codes, accumulators and outputs as the original layer
+on whole rows.  CPU: the oracle on both parameterisations (product `split_packed` vs bench-local
+`_split_packed` vs the plain gather of the oracle's own columns).  GPU: the product kernels on
+packed rows against the oracle on whole rows, bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import fit as ofit
+
+
+def _case(seed, N, D, M, C, dtype="f32"):
+    w = synth.small_case(seed, N=N, D=D, M=M, C=C, dtype=dtype, n_train=600)
+    params = ofit.fit(w["A_train"], w["B"], C, w["perm"], w["bias"], a_is_bf16=dtype == "bf16")
+    return w, params
+
+
+@pytest.mark.parametrize("seed,N,D,M,C,dtype", [(31, 300, 97, 33, 10, "f32"), (32, 257, 784, 64, 32, "f32"),
+                                                (33, 200, 300, 20, 75, "bf16")])
+def test_packed_layer_equals_whole_row_layer_oracle(seed, N, D, M, C, dtype):
+    from paper_2207_05808_b200 import split_packed
+    import bench
+    w, params = _case(seed, N, D, M, C, dtype)
+    pp, cols = split_packed(params)
+    pp2, cols2 = bench._split_packed(params)
+    assert np.array_equal(cols, cols2) and pp["D"] == pp2["D"] == 4 * C
+    assert cols.shape == (4 * C,) and cols.min() >= 0 and cols.max() < D
+    A = w["A"]
+    ref = oracle.amm(params, A, relu=w["relu"], dtype=dtype, want_codes=True, want_acc=True)
+    got = oracle.amm(pp, np.ascontiguousarray(A[:, cols]), relu=w["relu"], dtype=dtype, want_codes=True,
+                     want_acc=True)
+    assert np.array_equal(got["codes"], ref["codes"])
+    assert np.array_equal(got["acc"], ref["acc"])
+    assert np.array_equal(got["y"].view(np.uint32), ref["y"].view(np.uint32))
+
+
+def test_split_columns_follow_the_permutation_and_partition():
+    """cols[c][t] = perm[b_c + split_dim[c][t]] with larger-first chunks (reading R12)."""
+    from paper_2207_05808_b200.fit import split_columns, chunk_bounds
+    D, C = 10, 3
+    perm = np.array([9, 8, 7, 6, 5, 4, 3, 2, 1, 0])
+    sd = np.array([[0, 1, 2, 3], [2, 1, 0, 0], [0, 2, 1, 2]])
+    cols = split_columns(dict(D=D, C=C, perm=perm, boundaries=None, split_dim=sd))
+    b = chunk_bounds(D, C)
+    assert list(b) == [0, 4, 7, 10]
+    assert list(cols) == [9, 8, 7, 6, 3, 4, 5, 5, 2, 0, 1, 0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["auto", "tc", "simt"])
+def test_packed_rows_on_gpu_match_whole_row_oracle(algo):
+    torch = pytest.importorskip("torch")
+    from paper_2207_05808_b200 import Plan, split_packed
+    from paper_2207_05808_b200._lib import ItlummError
+    w, params = _case(34, 3001, 784, 512, 32)
+    pp, cols = split_packed(params)
+    ref = oracle.amm(params, w["A"], relu=True, want_codes=True, want_acc=True, nthreads=8)
+    plan = Plan(pp, device=0)
+    try:
+        plan.set_algo(algo)
+        A = torch.from_numpy(np.ascontiguousarray(w["A"][:, cols])).cuda()
+        y = plan.amm(A, relu=True)
+    except ItlummError as e:
+        if e.status == 3:
+            pytest.skip(str(e))
+        raise
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref["y"].view(np.uint32))

@@ -56,6 +56,7 @@ def main():
     ap.add_argument("--only", default="encode,acc,fused")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--summation", default="exact")
+    ap.add_argument("--packed", action="store_true", help="split-packed input (the layer re-parameterised)")
     args = ap.parse_args()
     global GRAPH
     GRAPH = not args.no_graph
@@ -64,6 +65,10 @@ def main():
     bf16 = cfg["dtype"] == "bf16"
     w = synth.workload(args.workload, n_rows=n)
     params = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
+    if args.packed:
+        from paper_2207_05808_b200 import split_packed
+        params, cols = split_packed(params)
+        w["A"] = np.ascontiguousarray(w["A"][:, cols])
     plan = Plan(params)
     if args.summation != "exact":
         plan.set_summation(args.summation)
