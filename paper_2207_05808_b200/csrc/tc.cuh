@@ -433,6 +433,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
             mbar_wait(empty_bar + stage, phase ^ 1);
             mbar_arrive_expect_tx(full_bar + stage, bbytes);
             bulk_g2s(b_s + (size_t)stage * bbytes, src + (size_t)kb * bbytes, bbytes, full_bar + stage);
+            stamp(3);
             if (++stage == ST) { stage = 0; phase ^= 1; }
           }
         }
@@ -595,6 +596,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
             umma_i8(d, ad + 6, bd + 6, idesc, 1u);
           }
           umma_commit(empty_bar + stage);             // frees the stage when these MMAs finish
+          stamp(1);
           if (kb == KB - 1) umma_commit(accf_bar + acc);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }

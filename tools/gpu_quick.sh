@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_split_packed.py -q -m gpu --timeout 300 > gpurun_out/enc2_tests.txt 2>&1; tail -1 gpurun_out/enc2_tests.txt
-for w in cfg2 cfg2_packed cfg3_c64 cfg3_c128; do timeout 600 python bench.py --workload $w --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$w', round(d['ms_per_step']*1e3,2), round(d['roofline']['frac'],3), [(k['kernel'][:8], round(k['ms']*1e3,1)) for k in d['roofline']['kernels']])" >> gpurun_out/quick.txt; done
-for w in cfg4_c64 cfg4_c256; do timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$w', round(d['ms_per_step']*1e3,2), round(d['roofline']['frac'],3))" >> gpurun_out/quick.txt; done
+for e in "X=0" "ITLUMM_OUT_HINT=85" "X=0" "ITLUMM_OUT_HINT=85"; do for w in cfg2 cfg5; do env $e timeout 300 python tools/kbench.py --workload $w --algos tc --only acc --iters 20 | sed "s/^/$e /" >> gpurun_out/quick.txt; done; done

@@ -59,6 +59,17 @@ for cta in range(4):
     print("  mma      ", mm[:30].tolist())
     print("  epi s/e  ", ep.tolist())
     print("  end      ", max(pk.max(initial=0), mm.max(initial=0), ep.max(initial=0)))
+if len(sys.argv) > 3 and sys.argv[3] == "cadence":
+    # streamed LUT: per K-block, loader B-issue (role 3, after the item's codes stamp), producer
+    # arrive (role 0) and MMA issue (role 1, after the item stamp) of CTA 0
+    x = lambda r: (t[0, r][t[0, r] > 0] - t0)
+    ld, pk, mm = x(3), x(0), x(1)
+    print("loader stamps (codes+B):", np.diff(ld[:40]).tolist())
+    print("producer K-block deltas:", np.diff(pk[:40]).tolist())
+    print("mma stamp deltas:       ", np.diff(mm[:40]).tolist())
+    n = min(len(pk), 300)
+    print("median producer cadence (ns):", float(np.median(np.diff(pk[50:n]))))
+    print("median mma cadence (ns):", float(np.median(np.diff(mm[50:min(len(mm), 300)]))))
 for cta in range(8, 10):
     pi, cd, pu = (t[cta, r][t[cta, r] > 0] - t0 for r in range(3))
     print(f"encoder CTA {cta - 8}: issues {len(pi)}, consumed {len(cd)}, published {len(pu)}")
