@@ -93,6 +93,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def i8_peak():
+    """Dense int8 tensor peak for the one-hot x LUT contraction: the measured bf16 GEMM burst
+    (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio 2 (4.5 / 2.25 PFLOP/s dense)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return 2.0 * float(d["bf16_tflops"]), "measured bf16 burst (MEASURED_PEAKS.json) x 2 (int8/bf16 nominal ratio)"
+    return 2.0 * 1590.0, "fallback (B200_PROFILING.md: 1.59 PF bf16) x 2"
+
+
 def alg_bytes(w: dict, n: int) -> int:
     """A split columns + output + LUT = N*(4C*s_A + 4M) + 16CM per launch."""
     s_a = 2 if w["dtype"] == "bf16" else 4
@@ -287,6 +298,14 @@ def run_ours(args):
              "achieved_GBps": b_acc / (t_acc * 1e-3) / 1e9},
         ]
         del g_enc, g_acc
+        # the accumulate's other roofline (SURVEY 8(d) "tensor int8 ceiling = peak / (32 C M)"):
+        # the one-hot x LUT product is 2 * 16C * M int8 ops per row
+        pk, pk_src = i8_peak()
+        ops = 32.0 * cfg["C"] * cfg["M"] * n
+        kernels[1]["tensor"] = {"bound": "tensor", "achieved": ops / (t_acc * 1e-3) / 1e12, "peak": pk,
+                                "unit": "TOPS (int8, dense-equivalent one-hot MMA work)",
+                                "frac": ops / (t_acc * 1e-3) / 1e12 / pk, "peak_source": pk_src,
+                                "ops_per_launch": ops}
 
     # end to end through the host-buffer C-ABI call (H2D + kernel + D2H inside the region)
     out_pin = torch.empty((n, cfg["M"]), dtype=torch.float32).pin_memory()
@@ -337,11 +356,21 @@ def run_ours(args):
                          "peak_source": peak_src,
                          "kernel": f"itlumm_amm ({per_step_launches} kernel launch(es) per call)",
                          "kernels": kernels},
+            # when the tensor-core accumulate dominates the call and sits closer to its int8 roofline
+            # than the call to HBM (streamed-LUT shapes), that is the roofline that binds
+            "roofline_tensor": (kernels[1]["tensor"] if kernels else None),
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
+        if kernels and kernels[1]["ms"] > kernels[0]["ms"] and kernels[1]["tensor"]["frac"] > line["roofline"]["frac"]:
+            hbm = line["roofline"]
+            tr = dict(kernels[1]["tensor"])
+            tr.update(kernel="k_tc (dominant kernel of the call: one-hot x LUT on tcgen05 + dequant)",
+                      launch_ms=kernels[1]["ms"], traffic=None, kernels=kernels)
+            line["roofline"] = tr
+            line["roofline_hbm"] = {k: v for k, v in hbm.items() if k != "kernels"}
     plan.close()
     if world > 1:
         dist.destroy_process_group()

@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_split_packed.py -q -m gpu --timeout 120 -x > gpurun_out/dyn_tests.txt 2>&1; tail -3 gpurun_out/dyn_tests.txt
-for e in "ITLUMM_TC_DYN=0" "X=0" "ITLUMM_TC_DYN=0" "X=0"; do for w in cfg2 cfg2_packed; do env $e timeout 300 python bench.py --workload $w --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$e $w', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done; done
-for e in "ITLUMM_TC_DYN=0" "X=0"; do for w in cfg3_c64 cfg1; do env $e timeout 300 python bench.py --workload $w --steps 200 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$e $w', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done; for w in cfg5 cfg4_c16 cfg4_c256; do env $e timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$e $w', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done; done
-python tools/span_trace.py cfg2 >> gpurun_out/quick.txt 2>&1
+for w in cfg2 cfg3_c128 cfg5; do timeout 600 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/rt_$w.json 2>gpurun_out/rt_$w.err; done
