@@ -42,3 +42,22 @@ print(f"TC CTAs {len(tc)}: start {f(tc[:, 0].min())}..{f(tc[:, 0].max())} us, en
 print("encoder end percentiles (us):", f(np.percentile(enc[:, 1], [0, 10, 50, 90, 100])))
 print("TC start percentiles (us):", f(np.percentile(tc[:, 0], [0, 10, 50, 90, 100])))
 print("TC end percentiles (us):", f(np.percentile(tc[:, 1], [0, 10, 50, 90, 100])))
+if len(sys.argv) > 2 and sys.argv[2] == "detail":
+    # per TC CTA: start, end, duration; CTAs with a leftover column part (static schedule:
+    # worker = cta // G < rem * parts) vs without
+    tcs = sp[1]
+    idx = np.nonzero(tcs[:, 0] > 0)[0]
+    G = int(os.environ.get("TC_G", "2"))
+    ntiles = (cfg["N"] + 127) // 128
+    ngroups = len(idx) // G
+    full, rem = ntiles // ngroups, ntiles % ngroups
+    parts = max(1, min(cfg["M"] // G // 32, ngroups // rem)) if rem else 1
+    lead = (idx // G) < rem * parts
+    st, en = tcs[idx, 0], tcs[idx, 1]
+    print(f"G={G} ngroups={ngroups} full={full} rem={rem} parts={parts}")
+    for nm, m in (("with part", lead), ("without", ~lead)):
+        print(f"  {nm:10s}: n={m.sum():3d} start {f(st[m].mean())} end {f(en[m].mean())} (max {f(en[m].max())}) "
+              f"dur {np.round((en[m] - st[m]).mean() / 1000.0, 2)} us")
+    order = np.argsort(en)
+    print("  latest 10 CTAs (cta, start, end):", [(int(idx[i]), float(f(st[i])), float(f(en[i]))) for i in order[-10:]])
+    print("  corr(start, end):", float(np.corrcoef(st, en)[0, 1]))
