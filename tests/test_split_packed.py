@@ -68,3 +68,28 @@ def test_packed_rows_on_gpu_match_whole_row_oracle(algo):
         raise
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy().view(np.uint32), ref["y"].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,N,D,M,C,dtype", [(35, 2500, 512, 300, 64, "bf16"), (36, 1300, 1024, 96, 128, "f32"),
+                                                (37, 777, 300, 40, 48, "f32")])
+def test_packed_rows_register_tree_walk_paths(seed, N, D, M, C, dtype):
+    """Split-packed rows through the encoder's register-threshold path (fixed codebook groups:
+    C = 64 bf16 vector loads of 8 bytes, C = 128 f32, C = 48 with a partly empty second group)."""
+    torch = pytest.importorskip("torch")
+    from paper_2207_05808_b200 import Plan, split_packed
+    w, params = _case(seed, N, D, M, C, dtype)
+    pp, cols = split_packed(params)
+    ref = oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, want_codes=True, nthreads=8)
+    plan = Plan(pp, device=0)
+    Ap = np.ascontiguousarray(w["A"][:, cols])
+    A = torch.from_numpy(Ap.view(np.int16) if dtype == "bf16" else Ap).cuda()
+    if dtype == "bf16":
+        A = A.view(torch.bfloat16)
+    codes = plan.encode(A)
+    y = plan.amm(A, relu=w["relu"])
+    torch.cuda.synchronize()
+    c = codes.cpu().numpy()
+    got = np.stack([(c[:, i // 2] >> (4 * (i % 2))) & 15 for i in range(C)], axis=1)
+    assert np.array_equal(got, ref["codes"])
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref["y"].view(np.uint32))
