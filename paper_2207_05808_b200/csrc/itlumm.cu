@@ -450,7 +450,10 @@ static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2,
   // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
   // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
   // ITLUMM_ENC_STAGE_KB, ITLUMM_ENC_INFLIGHT_KB.
-  static const int stage_kb = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 24;
+  // 48 KB stages where the consumers are compute-heavy (C >= 128: the per-tile handshake is amortised
+  // over twice the rows; D=592 C=256 encode 294 -> 263 us)
+  static const int stage_kb_env = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 0;
+  const int stage_kb = stage_kb_env > 0 ? stage_kb_env : (P->C >= 128 ? 48 : 24);
   static const int inflight_kb = getenv("ITLUMM_ENC_INFLIGHT_KB") ? atoi(getenv("ITLUMM_ENC_INFLIGHT_KB")) : 100;
   if (rb > 64 * 1024) return false;
   const int ngrp = (P->C + 31) / 32;

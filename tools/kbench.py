@@ -60,10 +60,17 @@ def main():
     args = ap.parse_args()
     global GRAPH
     GRAPH = not args.no_graph
-    cfg = synth.CONFIGS[args.workload]
-    n = cfg["N"] if args.rows is None else args.rows
-    bf16 = cfg["dtype"] == "bf16"
-    w = synth.workload(args.workload, n_rows=n)
+    if args.workload.startswith("shape:"):          # shape:N,D,M,C (synthetic small_case, f32, ReLU)
+        N_, D_, M_, C_ = (int(x) for x in args.workload[6:].split(","))
+        cfg = dict(N=N_, M=M_, C=C_, relu=True, dtype="f32")
+        n = N_
+        bf16 = False
+        w = synth.small_case(77, N=N_, D=D_, M=M_, C=C_, n_train=2000)
+    else:
+        cfg = synth.CONFIGS[args.workload]
+        n = cfg["N"] if args.rows is None else args.rows
+        bf16 = cfg["dtype"] == "bf16"
+        w = synth.workload(args.workload, n_rows=n)
     params = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
     if args.packed:
         from paper_2207_05808_b200 import split_packed
