@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-for cfg in "24 100" "16 100" "32 100" "24 80" "24 130" "24 160" "32 128" "48 144"; do set -- $cfg
-  ITLUMM_ENC_STAGE_KB=$1 ITLUMM_ENC_INFLIGHT_KB=$2 timeout 300 python bench.py --steps 500 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('stage=$1 infl=$2', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt
-done
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_split_packed.py -q -m gpu --timeout 120 -x > gpurun_out/ring_tests.txt 2>&1; tail -1 gpurun_out/ring_tests.txt
+for e in "ITLUMM_TC_STAGES=4 ITLUMM_TC_BSTAGES=4" "X=0" "ITLUMM_TC_STAGES=5 ITLUMM_TC_BSTAGES=3" "ITLUMM_TC_STAGES=4 ITLUMM_TC_BSTAGES=3" "ITLUMM_TC_STAGES=6 ITLUMM_TC_BSTAGES=2"; do for w in cfg3_c128 cfg5; do env $e timeout 300 python tools/kbench.py --workload $w --algos tc --only acc --iters 10 | sed "s/^/$e /" >> gpurun_out/quick.txt; done; done
