@@ -14,10 +14,16 @@ import synth  # noqa: E402
 from paper_2207_05808_b200 import Plan, fit_layer, _lib  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-cfg = synth.CONFIGS[name]
-w = synth.workload(name, n_rows=cfg["N"])
+packed = name.endswith("_packed")
+base = name[:-7] if packed else name
+cfg = synth.CONFIGS[base]
+w = synth.workload(base, n_rows=cfg["N"])
 bf16 = cfg["dtype"] == "bf16"
 p = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
+if packed:
+    from paper_2207_05808_b200 import split_packed
+    p, cols = split_packed(p)
+    w["A"] = np.ascontiguousarray(w["A"][:, cols])
 plan = Plan(p, algo="tc_pipe")
 A = torch.from_numpy(w["A"].view(np.int16) if bf16 else w["A"]).cuda()
 if bf16:
