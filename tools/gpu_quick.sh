@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-for e in 81 100 116 128; do ITLUMM_SP_ENC_CTAS=$e timeout 300 python bench.py --workload cfg2 --algo tc_sp --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('cfg2 E=$e', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done
-for e in 25 40 55 70 90; do ITLUMM_SP_ENC_CTAS=$e timeout 300 python bench.py --workload cfg2_packed --algo tc_sp --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('cfg2_packed E=$e', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_split_packed.py -q -m gpu --timeout 120 -x -k "tc" > gpurun_out/i2f_tests.txt 2>&1; tail -1 gpurun_out/i2f_tests.txt
+for i in 1 2; do for w in cfg2 cfg5; do timeout 300 python tools/kbench.py --workload $w --algos tc --only acc --iters 30 >> gpurun_out/quick.txt; done; done
+for w in cfg2 cfg2_packed; do timeout 300 python bench.py --workload $w --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('$w', round(d['ms_per_step']*1e3,2))" >> gpurun_out/quick.txt; done
