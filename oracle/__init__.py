@@ -99,20 +99,6 @@ def amm(params: dict, A: np.ndarray, relu: bool, dtype: str = "f32", want_codes:
     return dict(codes=codes, acc=acc, y=y)
 
 
-def pack_codes(codes: np.ndarray) -> np.ndarray:
-    """Nibble-pack [N][C] codes per reading R14 ("log2(K)-bit integer indices"):
-    byte c//2 holds code 2i in its low nibble and code 2i+1 in its high nibble; an odd C
-    leaves the last high nibble 0."""
-    N, C = codes.shape
-    out = np.zeros((N, (C + 1) // 2), dtype=np.uint8)
-    for c in range(C):
-        if c % 2 == 0:
-            out[:, c // 2] |= codes[:, c]
-        else:
-            out[:, c // 2] |= (codes[:, c] << 4).astype(np.uint8)
-    return out
-
-
 def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, relus: list,
             a_is_bf16: bool = False, nthreads: int = 8) -> list:
     """Fit an MLP whose linear layers are all ITLUMM (BASELINE configs[3]): layer l+1

@@ -233,6 +233,16 @@ def test_quantize_golden_examples():
         assert np.array_equal(qq[0, :, 0] * sc[0] + lo[0], T[0, :, 0]), name
 
 
+def test_quantize_ties_round_half_up():
+    """Reading R6 at exact .5 ties (golden file tests/golden/quantize_ties_r6.txt): the
+    quantiser rounds half UP, so half-to-even or truncation would fail here."""
+    for name, vals, scale, q in read_golden("quantize_ties_r6.txt"):
+        T = np.array([float(x) for x in vals.split()]).reshape(1, 16, 1)
+        qq, sc, lo = ofit.quantize(T)
+        assert sc[0] == float(scale), name
+        assert np.array_equal(qq[0, :, 0], [int(x) for x in q.split()]), name
+
+
 def test_quantize_error_bound():
     """|q*scale + lo - T| <= scale/2 elementwise; q uses the full [0,255] range."""
     g = np.random.default_rng(2)
@@ -366,6 +376,35 @@ def test_exact_pq_end_to_end():
     assert np.abs(out["y"] - exact).max() > 0  # quantisation is actually exercised
 
 
+def test_exact_pq_end_to_end_shuffled_permutation():
+    """Exact PQ through a NON-identity permutation (P:62 a'[i] = a[perm[i]], reading R11): the
+    patterns live in the permuted coordinates, the raw rows scatter them (a[perm] = a'), and B
+    stays in the raw coordinates.  The fit must build chunk c's LUT from the rows B[perm[b_c:b_c+1]],
+    so y matches a.B + bias within C*scale/2; a LUT built from the unpermuted rows
+    B[b_c:b_c+1] misses that bound (checked, so this test can tell the two apart)."""
+    C, M = 6, 9
+    Ap_train, Ap_test, kt, B, bias = exact_pq_case(C, M, seed=3)
+    D = 4 * C
+    perm = np.random.default_rng(11).permutation(D)
+    assert not np.array_equal(perm, np.arange(D))
+    A_train = np.zeros_like(Ap_train)
+    A_train[:, perm] = Ap_train
+    A_test = np.zeros_like(Ap_test)
+    A_test[:, perm] = Ap_test
+    p = ofit.fit(A_train, B, C, perm, bias)
+    assert np.array_equal(p["split_dim"], np.tile([0, 1, 2, 3], (C, 1)))
+    assert np.all(p["thresholds"] == 0)
+    out = oracle.amm(p, A_test, relu=False, want_codes=True)
+    assert np.array_equal(out["codes"], kt)
+    exact = A_test.astype(np.float64) @ B + bias.astype(np.float64)
+    bound = C * p["scale64"] / 2 + 1e-5 * (1 + np.abs(exact))
+    assert np.all(np.abs(out["y"] - exact) <= bound)
+    # the misreading (LUT from unpermuted rows of B) is far outside the bound
+    b = p["boundaries"]
+    wrong = sum(p["prototypes"][c][kt[:, c]] @ B[b[c]:b[c + 1]] for c in range(C)) + bias
+    assert np.any(np.abs(wrong - exact) > bound)
+
+
 def test_fit_lut_size_and_code_range_invariants():
     """LUT = 16*C*M bytes; codes in [0,16); leaf sizes sum to n_train (BASELINE)."""
     w = synth.small_case(1, N=200, D=64, M=24, C=8)
@@ -459,6 +498,23 @@ def test_eq3_linear_single_codebook_is_bucket_ridge_mean():
         rows = codes[:, 0] == k
         want = (Y[rows].sum(axis=0) + lam * T0[0, k]) / (rows.sum() + lam)
         assert np.allclose(T[0, k], want, rtol=1e-12, atol=1e-12)
+
+
+def test_eq3_objective_hand_computed():
+    """eq3_objective (sigma = bias then optional ReLU) on a case worked by hand:
+    A = [[1],[2]], B = [[3]] -> AB = [3, 6]; codes [[0],[1]]; T[0][0] = 2.5, T[0][1] = 7 (rest 0)
+    -> GT = [2.5, 7]; T0[0][0] = 2 (rest 0), lam = 0.1 -> lam*||T - T0||^2 = 0.1*(0.25 + 49) = 4.925.
+    bias 0.5: sigma(AB) = [3.5, 6.5], sigma(GT) = [3.0, 7.5] -> 0.25 + 1 = 1.25; total 6.175.
+    bias -4 with ReLU: [-1, 2] -> [0, 2] and [-1.5, 3] -> [0, 3] -> 1; total 5.925."""
+    A = np.array([[1.0], [2.0]])
+    B = np.array([[3.0]])
+    codes = np.array([[0], [1]], np.uint8)
+    T = np.zeros((1, 16, 1))
+    T[0, 0, 0], T[0, 1, 0] = 2.5, 7.0
+    T0 = np.zeros((1, 16, 1))
+    T0[0, 0, 0] = 2.0
+    assert ofit.eq3_objective(A, B, np.array([0.5]), codes, T, T0, 0.1, relu=False) == pytest.approx(6.175, abs=1e-12)
+    assert ofit.eq3_objective(A, B, np.array([-4.0]), codes, T, T0, 0.1, relu=True) == pytest.approx(5.925, abs=1e-12)
 
 
 def test_eq3_linear_optimality_and_limits():
