@@ -615,7 +615,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
-    ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc", "tc_pipe", "tc_sp"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc", "tc_pipe"])
     ap.add_argument("--rows", type=int, default=None, help="override rows per GPU (default: config N)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -36,12 +36,14 @@
 extern "C" {
 #endif
 
-#define ITLUMM_ABI_VERSION 4
+#define ITLUMM_ABI_VERSION 5
 
 typedef enum {
   ITLUMM_OK = 0,
   ITLUMM_EINVAL = 1,        /* bad argument: null pointer, bad size/stride, invalid parameters */
-  ITLUMM_ESHAPE = 2,        /* call inconsistent with the plan ("shape mismatch") */
+  ITLUMM_ESHAPE = 2,        /* call inconsistent with the plan's dims ("shape
+                               mismatch"): lda < D, ldc < ceil(C/2), ldo or ldacc < M, or an MLP
+                               whose layer l+1 has D != M of layer l                           */
   ITLUMM_EUNSUPPORTED = 3,  /* shape/dtype/alignment the selected kernel cannot take          */
   ITLUMM_ECUDA = 4,         /* CUDA launch/config/runtime failure (cudaGetErrorString in msg) */
   ITLUMM_ENOMEM = 5         /* device or host allocation failure                             */
@@ -52,24 +54,22 @@ typedef enum { ITLUMM_EPI_NONE = 0, ITLUMM_EPI_RELU = 1 } itlumm_epilogue;  /* s
 
 /* Kernel schedule used by itlumm_amm / itlumm_amm_host / itlumm_lut_accumulate.
  *   AUTO    : library choice: TC_PIPE (itlumm_amm) / TC
- *             (itlumm_lut_accumulate) where the tensor-core tiling applies, else SIMT.
+ *             (itlumm_lut_accumulate) where the tensor-core tiling applies, else SIMT.  If a
+ *             tensor-core kernel cannot take the codes it is given (a streamed LUT needs codes rows
+ *             that are 16-byte multiples), itlumm_lut_accumulate runs the SIMT kernel instead.
  *   SIMT    : CUDA-core shared-memory LUT kernels; itlumm_amm = one fused kernel.
  *   TC      : tcgen05 one-hot x LUT int8 tensor-core kernel (G.T with G the one-hot encoding,
- *             P:89; exact integer products); itlumm_amm = one fused kernel (encode inside).
+ *             P:89; exact integer products); itlumm_amm = one fused kernel (encode inside) where the
+ *             LUT stays resident in shared memory.
  *   TC_PIPE : itlumm_amm = the encode kernel writing codes to a plan-owned, L2-resident scratch
  *             buffer, then the TC accumulate kernel (2 launches; concurrent calls on one plan
  *             are serialised on the device through an event).  itlumm_lut_accumulate = TC.
- *   TC_SP   : itlumm_amm = ONE cooperative launch, one CTA per SM, spatially partitioned: E
- *             CTAs encode (rows streamed by TMA) into the plan's L2-resident code buffer while
- *             the other CTAs run the TC accumulate on codes tiles as they become ready (per-tile
- *             ready counters; no CTA of the TC side can block an encoder).  Same serialisation of
- *             concurrent calls as TC_PIPE.  itlumm_lut_accumulate = TC.  Falls back to TC_PIPE
- *             where rows cannot be bulk-copied or cooperative launch is unavailable.
+ * Where the LUT is too large to stay resident (it is then streamed K-block by K-block), the TC
+ * accumulate runs on CTA pairs (tcgen05.mma.cta_group::2, each SM stages half of every LUT block).
  * TC and TC_PIPE return EUNSUPPORTED where the tensor-core tiling does not apply.  Every
  * schedule produces bit-identical results. */
 typedef enum {
-  ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2, ITLUMM_ALGO_TC_PIPE = 3,
-  ITLUMM_ALGO_TC_SP = 4
+  ITLUMM_ALGO_AUTO = 0, ITLUMM_ALGO_SIMT = 1, ITLUMM_ALGO_TC = 2, ITLUMM_ALGO_TC_PIPE = 3
 } itlumm_algo;
 
 /* Summation over codebooks (a3).
@@ -83,13 +83,14 @@ typedef enum {
 typedef enum { ITLUMM_SUM_EXACT = 0, ITLUMM_SUM_AVG16 = 1 } itlumm_summation;
 
 /* Operand form of the one-hot matrix G on the tensor-core paths (TC, TC_PIPE).
+ *   AUTO     : library choice: DENSE (the 2:4-sparse form measured slower on every kernel,
+ *              DESIGN.md §7.2).
  *   DENSE    : G as u8 (16 bytes per codebook), tcgen05.mma kind::i8, K = 32 per instruction.
  *   SPARSE24 : G is 1-of-16 per codebook, hence 2:4 sparse: stored compressed (8 bytes per
  *              codebook) with 2-bit position metadata per stored element, tcgen05.mma.sp kind::i8,
  *              K = 64 per instruction; N slices of at most 224 columns (TMEM holds the metadata).
- * Both give the same exact integer products (bit-identical results).  TC_SP and the CTA-pair
- * kernel run DENSE (TC_SP with SPARSE24 runs as TC_PIPE). */
-typedef enum { ITLUMM_ONEHOT_DENSE = 0, ITLUMM_ONEHOT_SPARSE24 = 1 } itlumm_onehot;
+ * All give the same exact integer products (bit-identical results). */
+typedef enum { ITLUMM_ONEHOT_AUTO = 0, ITLUMM_ONEHOT_DENSE = 1, ITLUMM_ONEHOT_SPARSE24 = 2 } itlumm_onehot;
 
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */
 
@@ -129,7 +130,7 @@ itlumm_status itlumm_plan_set_algo(itlumm_plan plan, itlumm_algo algo);
  * thread-safe against concurrent launches. */
 itlumm_status itlumm_plan_set_summation(itlumm_plan plan, itlumm_summation summation);
 
-/* Select the one-hot operand form (default DENSE).  EUNSUPPORTED when the tensor-core tiling of
+/* Select the one-hot operand form (default AUTO).  EUNSUPPORTED when the tensor-core tiling of
  * that form does not apply to the plan.  Not thread-safe against concurrent launches. */
 itlumm_status itlumm_plan_set_onehot(itlumm_plan plan, itlumm_onehot onehot);
 
@@ -140,14 +141,16 @@ itlumm_status itlumm_plan_info(itlumm_plan plan, int32_t* D, int32_t* C, int32_t
 /* a1 + a2.  A: device, N rows x lda elements of `dtype`, row-major, lda >= D; only the 4C
  * split columns of each row are read.  codes: device, N x ldc bytes, ldc >= ceil(C/2);
  * row r byte i holds code 2i in its low nibble and code 2i+1 in its high nibble (R14; an odd
- * C leaves the last high nibble 0).  Errors: EINVAL (null, N < 0, lda < D, ldc < ceil(C/2),
- * bad dtype), ECUDA. */
+ * C leaves the last high nibble 0).  Errors: EINVAL (null, N < 0, bad dtype, A or codes not device
+ * memory of the plan's device), ESHAPE (lda < D, ldc < ceil(C/2)), ECUDA. */
 itlumm_status itlumm_encode(itlumm_plan plan, const void* A, itlumm_dtype dtype, int64_t lda,
                             int64_t N, uint8_t* codes, int64_t ldc, void* stream);
 
 /* a3 (+ a4).  codes as produced by itlumm_encode.  acc: device int32 [N][ldacc] (ldacc >= M)
  * or NULL; out: device fp32 [N][ldo] (ldo >= M) or NULL; at least one must be non-NULL.
- * `epi` applies to `out` only.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+ * `epi` applies to `out` only.  Errors: EINVAL (null codes, both outputs NULL, a pointer that is
+ * not device memory of the plan's device), ESHAPE (ldc < ceil(C/2), ldacc or ldo < M),
+ * EUNSUPPORTED, ECUDA. */
 itlumm_status itlumm_lut_accumulate(itlumm_plan plan, const uint8_t* codes, int64_t ldc,
                                     int64_t N, int32_t* acc, int64_t ldacc, float* out,
                                     int64_t ldo, itlumm_epilogue epi, void* stream);
@@ -155,7 +158,8 @@ itlumm_status itlumm_lut_accumulate(itlumm_plan plan, const uint8_t* codes, int6
 /* a1..a4 in one call.  With SIMT/TC one fused kernel (codes never leave the SM); with
  * TC_PIPE (AUTO's choice when M is split across CTAs) encode + accumulate kernels exchanging
  * the codes (ceil(C/2) bytes per row) through an L2-resident scratch buffer.  A as in
- * itlumm_encode, out device fp32 [N][ldo], ldo >= M.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+ * itlumm_encode, out device fp32 [N][ldo], ldo >= M.  Errors: EINVAL (null, N < 0, bad dtype, A or
+ * out not device memory of the plan's device), ESHAPE (lda < D, ldo < M), EUNSUPPORTED, ECUDA. */
 itlumm_status itlumm_amm(itlumm_plan plan, const void* A, itlumm_dtype dtype, int64_t lda,
                          int64_t N, float* out, int64_t ldo, itlumm_epilogue epi, void* stream);
 
@@ -181,8 +185,8 @@ typedef struct itlumm_mlp_s* itlumm_mlp; /* opaque; owns one plan per layer + in
 
 /* layers[l]: host params as for itlumm_plan_create (read during the call only); requires
  * layers[l+1].D == layers[l].M.  epis[l]: sigma of layer l (ReLU on hidden layers).
- * Errors: as itlumm_plan_create (message prefixed with the layer index), EINVAL on a shape chain
- * mismatch or n_layers < 1. */
+ * Errors: as itlumm_plan_create (message prefixed with the layer index), ESHAPE on a shape chain
+ * mismatch, EINVAL on n_layers < 1. */
 itlumm_status itlumm_mlp_create(const itlumm_params* layers, const itlumm_epilogue* epis,
                                 int32_t n_layers, int cuda_device, itlumm_mlp* out);
 
@@ -196,7 +200,7 @@ itlumm_status itlumm_mlp_info(itlumm_mlp mlp, int32_t* n_layers, int32_t* widths
  * (ldo >= last layer's M).  Rows are processed in chunks of up to 262144 through plan-owned
  * intermediate buffers (allocated on first use: ENOMEM possible).  Async on `stream`; calls on one
  * MLP are serialised on the device by the stream order the caller gives them.
- * Errors: EINVAL, ENOMEM, EUNSUPPORTED, ECUDA. */
+ * Errors: EINVAL, ESHAPE (lda < layers[0].D, ldo < last M), ENOMEM, EUNSUPPORTED, ECUDA. */
 itlumm_status itlumm_mlp_forward(itlumm_mlp mlp, const void* A, itlumm_dtype dtype, int64_t lda,
                                  int64_t N, float* out, int64_t ldo, void* stream);
 

@@ -13,9 +13,9 @@ OK, EINVAL, ESHAPE, EUNSUPPORTED, ECUDA, ENOMEM = range(6)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA", 5: "ENOMEM"}
 F32, BF16 = 0, 1
 EPI_NONE, EPI_RELU = 0, 1
-ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3, "tc_sp": 4}
+ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3}
 SUMMATION = {"exact": 0, "avg16": 1}
-ONEHOT = {"dense": 0, "sparse24": 1}
+ONEHOT = {"auto": 0, "dense": 1, "sparse24": 2}
 
 # every symbol include/itlumm.h declares (checked by tests/test_abi.py against the header)
 EXPORTS = [

@@ -21,10 +21,31 @@ def _np_ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
-def _stream(stream):
+def _stream(stream, device):
+    """A raw cudaStream_t: `stream` (a torch.cuda.Stream or an int handle), else the current stream of
+    the plan's device."""
     if stream is not None:
-        return ctypes.c_void_p(int(stream))
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check(t, name, dtypes, rows, cols, device=None):
+    """Reject what the C ABI cannot detect from raw pointers: a tensor on the wrong device (or on the
+    host when device memory is required), the wrong element type, too few rows or columns, or rows
+    that are not unit-stride."""
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+    if device is None:
+        if t.is_cuda:
+            raise ValueError(f"{name} must be a host tensor")
+    elif not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{name} must live on cuda:{device}, got {t.device}")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} must be {' or '.join(str(d) for d in dtypes)}, got {t.dtype}")
+    if t.shape[0] < rows or t.shape[1] < cols:
+        raise ValueError(f"{name} is {tuple(t.shape)}, needs at least ({rows}, {cols})")
+    if t.shape[0] > 1 and t.stride(1) != 1 and t.shape[1] > 1:
+        raise ValueError(f"{name} rows must be contiguous (stride(1) == 1), got strides {t.stride()}")
 
 
 def _dtype_code(t):
@@ -55,6 +76,10 @@ def _params_struct(params: dict):
     return p, keep
 
 
+def _a_dtypes():
+    return (torch.float32, torch.bfloat16, torch.int16, torch.uint16)
+
+
 class Plan:
     """An immutable ITLUMM layer on one GPU (itlumm_plan)."""
 
@@ -66,7 +91,7 @@ class Plan:
         _lib.check(self._lib.itlumm_plan_create(ctypes.byref(p), int(device), ctypes.byref(h)))
         self._h = h
         self.D, self.C, self.M, self.device = D, C, M, int(device)
-        self.summation, self.onehot = "exact", "dense"
+        self.summation, self.onehot = "exact", "auto"
         self.set_algo(algo)
 
     def close(self):
@@ -90,8 +115,9 @@ class Plan:
         self.summation = summation
 
     def set_onehot(self, onehot: str):
-        """"dense" (default) or "sparse24": the one-hot operand of the tensor-core paths as a
-        compressed 2:4-sparse matrix (tcgen05.mma.sp); bit-identical results."""
+        """"auto" (default: the library's choice, currently dense), "dense" or "sparse24": the one-hot
+        operand of the tensor-core paths (tcgen05.mma.sp for the 2:4-sparse form, SURVEY f2);
+        bit-identical results."""
         _lib.check(self._lib.itlumm_plan_set_onehot(self._h, _lib.ONEHOT[onehot]))
         self.onehot = onehot
 
@@ -103,36 +129,47 @@ class Plan:
     def encode(self, A, codes=None, stream=None):
         """a1+a2: A [N, lda>=D] fp32/bf16 on the plan's device -> packed codes [N, ceil(C/2)] u8."""
         N = A.shape[0]
+        _dtype_code(A)
+        _check(A, "A", _a_dtypes(), 0, self.D, self.device)
         if codes is None:
             codes = torch.empty((N, (self.C + 1) // 2), dtype=torch.uint8, device=A.device)
+        _check(codes, "codes", (torch.uint8,), N, (self.C + 1) // 2, self.device)
         _lib.check(self._lib.itlumm_encode(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
                                            A.stride(0), N, ctypes.c_void_p(codes.data_ptr()),
-                                           codes.stride(0), _stream(stream)))
+                                           codes.stride(0), _stream(stream, self.device)))
         return codes
 
     def lut_accumulate(self, codes, out=None, acc=None, relu=False, want_out=True, stream=None):
         """a3(+a4): packed codes -> fp32 out [N, M] (and/or int32 acc [N, M])."""
         N = codes.shape[0]
+        _check(codes, "codes", (torch.uint8,), 0, (self.C + 1) // 2, self.device)
         if out is None and want_out:
             out = torch.empty((N, self.M), dtype=torch.float32, device=codes.device)
+        if out is not None:
+            _check(out, "out", (torch.float32,), N, self.M, self.device)
+        if acc is not None:
+            _check(acc, "acc", (torch.int32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_lut_accumulate(
             self._h, ctypes.c_void_p(codes.data_ptr()), codes.stride(0), N,
             ctypes.c_void_p(acc.data_ptr()) if acc is not None else None,
             acc.stride(0) if acc is not None else self.M,
             ctypes.c_void_p(out.data_ptr()) if out is not None else None,
             out.stride(0) if out is not None else self.M,
-            _lib.EPI_RELU if relu else _lib.EPI_NONE, _stream(stream)))
+            _lib.EPI_RELU if relu else _lib.EPI_NONE, _stream(stream, self.device)))
         return out, acc
 
     def amm(self, A, out=None, relu=False, stream=None):
         """Fused a1..a4: A [N, lda>=D] -> out [N, M] fp32 (codes never reach HBM)."""
         N = A.shape[0]
+        _dtype_code(A)
+        _check(A, "A", _a_dtypes(), 0, self.D, self.device)
         if out is None:
             out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
+        _check(out, "out", (torch.float32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_amm(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
                                         A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
                                         out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
-                                        _stream(stream)))
+                                        _stream(stream, self.device)))
         return out
 
     # ------------------------------------------------------------------ host-buffer call
@@ -140,12 +177,15 @@ class Plan:
         """End-to-end: HOST rows (torch CPU tensor, pinned is fastest) -> HOST out [N, M] fp32.
         Blocking; H2D / kernel / D2H are pipelined inside the library."""
         N = A.shape[0]
+        _dtype_code(A)
+        _check(A, "A", _a_dtypes(), 0, self.D)
         if out is None:
             out = torch.empty((N, self.M), dtype=torch.float32, pin_memory=A.is_pinned())
+        _check(out, "out", (torch.float32,), N, self.M)
         _lib.check(self._lib.itlumm_amm_host(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
                                              A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
                                              out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
-                                             _stream(stream)))
+                                             _stream(stream, self.device)))
         return out
 
 
@@ -176,11 +216,14 @@ class Mlp:
 
     def forward(self, A, out=None, stream=None):
         N = A.shape[0]
+        _dtype_code(A)
+        _check(A, "A", _a_dtypes(), 0, self.D, self.device)
         if out is None:
             out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
+        _check(out, "out", (torch.float32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_mlp_forward(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
                                                 A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
-                                                out.stride(0), _stream(stream)))
+                                                out.stride(0), _stream(stream, self.device)))
         return out
 
     def close(self):

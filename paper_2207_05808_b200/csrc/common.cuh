@@ -75,10 +75,62 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
-// Blocking wait for the phase with `parity` to complete.  try_wait suspends in hardware for a
-// bounded time per attempt; after ~2^26 attempts (seconds) the kernel traps, so a broken pipeline
-// protocol surfaces as a launch error instead of a hung GPU.
+// Blocking wait for the phase with `parity` to complete.  try_wait with a suspend-time hint parks
+// the thread in hardware until the phase completes (or 1 ms passes), so waiting warps do not spin
+// and take issue slots from the warps they wait for (a spinning wait made the k_tcp producers sharing
+// an SM sub-partition with them ~2x slower, tcp_trace in profiles/r02).  After ~5 s of waiting the
+// kernel traps, so a broken pipeline protocol surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
+    if (ok) return;
+    if (it > 5000u) __trap();
+  }
+}
+// Spin on mbarrier.test_wait (never suspends): lowest wake-up latency, costs issue slots.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (it > (1u << 30)) __trap();
+  }
+}
+// Non-blocking test of a phase (warp-uniform when all lanes test the same barrier).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+// For waits off the critical path (an epilogue waiting for a whole tile, a loader far ahead of its
+// consumers): test, then a plain timed sleep of `ns` before testing again.  A try_wait suspension
+// (NANOSLEEP.SYNCS) ends at ANY barrier event of the SM, and in a kernel whose barriers change every
+// few hundred cycles such a waiter spins: ncu counted 140M re-checks in one k_tcp launch, stealing
+// issue slots from the producer warps that share its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (it > (1u << 26)) __trap();
+  }
+}
+// try_wait without a suspend-time hint (the hardware's default suspension window).
+__device__ __forceinline__ void mbar_wait_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   for (uint32_t it = 0;; ++it) {
     asm volatile(
@@ -86,7 +138,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     if (ok) return;
-    if (it > (1u << 26)) __trap();
+    if (it > (1u << 28)) __trap();
   }
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -139,6 +191,17 @@ __device__ __forceinline__ uint64_t gtimer_ns() {
 }
 
 __device__ __forceinline__ float relu_pos0(float y) { return y > 0.0f ? y : 0.0f; }
+
+// One lane of a converged warp (elect.sync): the lane that issues a warp-uniform tcgen05 op.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+// (float)v for v < 2^23: the bits of 2^23 + v, minus 2^23 (both steps exact).  FMA pipe, not the
+// conversion unit (I2F runs on the XU pipe: ncu flagged it saturated in the r01 epilogue).
+__device__ __forceinline__ float u2f_exact(uint32_t v) { return __uint_as_float(v | 0x4B000000u) - 8388608.0f; }
+
 
 __device__ __forceinline__ void st_cs_f4(float* p, float a, float b, float c, float d) {
   __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));

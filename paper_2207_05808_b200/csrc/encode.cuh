@@ -42,7 +42,7 @@ __host__ __device__ inline size_t enc_smem_bytes(int C, int R, int S, int row_by
   size_t o = (size_t)S * R * row_bytes;
   o += (size_t)15 * C * 4 + (size_t)C * 16;
   o = (o + 15) & ~(size_t)15;
-  o += (size_t)3 * S * 8;
+  o += (size_t)2 * S * 8;
   return o;
 }
 
@@ -51,15 +51,13 @@ __host__ __device__ inline size_t enc_smem_bytes(int C, int R, int S, int row_by
 // walks the tree of codebook 32u+l, adjacent lanes pair their nibbles with one shuffle and the
 // even lane stores the byte.  No CTA-wide barrier in the loop: warps drift across stages freely.
 // One persistent encoder CTA (`cta` of `ncta`) with warp 0 as the bulk-copy producer and
-// blockDim/32 - 1 consumer warps.  ready != nullptr (spatial pipeline): once every consumer warp
-// is done with an encode tile, the producer thread adds 1 to ready[row0 / 128].
+// blockDim/32 - 1 consumer warps.
 // WIDE (C >= 32): a warp unit is one 32-codebook group of one row, units taken in turn; the
 // general (row, codebook) lane mapping below is compiled out (it measured slower for C = 256:
 // cfg4 layer-1 encode 685 -> 783 us, when both lived in one kernel).
 template <typename T, bool WIDE>
-__device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint8_t* smem, int cta, int ncta,
-                                        uint32_t* ready) {
-  const int nconsumer = (int)(blockDim.x >> 5) - (ready ? 2 : 1);   // warp 1 publishes when ready
+__device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint8_t* smem, int cta, int ncta) {
+  const int nconsumer = (int)(blockDim.x >> 5) - 1;
   const int C = p.C, R = g.R, S = g.S, rb = g.row_bytes;
   const int rs = rb / (int)sizeof(T);                 // staged row stride (elements)
   uint8_t* rows_s = smem;
@@ -67,7 +65,6 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   float* thr_s = reinterpret_cast<float*>(cols_s + 4 * C);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (((size_t)S * R * rb + (size_t)15 * C * 4 + (size_t)C * 16 + 15) & ~(size_t)15));
   uint64_t* empty = full + S;
-  uint64_t* pub = empty + S;         // ready != nullptr: stage's tile published (producer reuses after)
   const int64_t ntiles = (g.N + R - 1) / R;
   const char* A = reinterpret_cast<const char*>(g.A);
   const size_t ldab = (size_t)g.lda * sizeof(T);
@@ -75,7 +72,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
   if (g.span && threadIdx.x == 0) g.span[2 * cta] = gtimer_ns();
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, nconsumer); mbar_init(pub + s, 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, nconsumer); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < 15 * C; i += blockDim.x) thr_s[i] = __ldg(p.thr_t + i);
@@ -90,7 +87,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
       const uint64_t pol = l2_policy(g.a_hint);
       for (int64_t tile = cta; tile < ntiles; tile += ncta, ++k) {
         const int s = k % S;
-        if (k >= S) mbar_wait((ready ? pub : empty) + s, (uint32_t)(((k / S) - 1) & 1));
+        if (k >= S) mbar_wait(empty + s, (uint32_t)(((k / S) - 1) & 1));
         const int64_t r0 = tile * R;
         const int rows = (int)((g.N - r0) < R ? (g.N - r0) : R);
         uint8_t* dst = rows_s + (size_t)s * R * rb;
@@ -105,37 +102,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
     }
     return;
   }
-  if (ready && warp == 1) {
-    // Publisher: once every consumer warp is done with encode tile k (their mbarrier arrive
-    // releases their code stores at CTA scope), a GPU-scope fence makes those stores visible
-    // before ready[] is bumped; then pub[] hands the stage back to the producer (so this thread
-    // lags at most S tiles and the mbarrier parities stay aligned).  A thread of its own, so the
-    // fence never waits behind the producer's in-flight bulk loads; tiles that are already drained
-    // share one fence.
-    if (lane == 0) {
-      const int64_t nmine = ntiles > cta ? (ntiles - cta + ncta - 1) / ncta : 0;
-      auto drained = [&](int64_t j) {
-        uint32_t ok;
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(empty + (j % S))), "r"((uint32_t)((j / S) & 1)) : "memory");
-        return ok != 0;
-      };
-      for (int64_t k = 0; k < nmine;) {
-        mbar_wait(empty + (k % S), (uint32_t)((k / S) & 1));
-        int64_t k1 = k + 1;
-        while (k1 < nmine && k1 < k + S && drained(k1)) ++k1;
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        for (int64_t j = k; j < k1; ++j) {
-          atomicAdd(ready + (((cta + j * ncta) * R) >> 7), 1u);
-          mbar_arrive(pub + (j % S));
-        }
-        k = k1;
-      }
-    }
-    return;
-  }
-
-  const int cw = warp - (ready ? 2 : 1);
+  const int cw = warp - 1;
   // lanes per row: the codebooks of a row (rounded up to a power of two, >= 2 so that adjacent
   // lanes pair their nibbles, <= 32); a warp unit covers 32 / lpr rows (short rows, small C) or one
   // 32-codebook group of one row (C > 32)
@@ -290,7 +257,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
 template <typename T, bool WIDE>
 __global__ void __launch_bounds__(kEncThreads, 1) k_encode_rows(DevPlan p, EncArgs g) {
   extern __shared__ __align__(16) uint8_t smem_enc[];
-  enc_cta<T, WIDE>(p, g, smem_enc, blockIdx.x, gridDim.x, nullptr);
+  enc_cta<T, WIDE>(p, g, smem_enc, blockIdx.x, gridDim.x);
 }
 
 }  // namespace itlumm

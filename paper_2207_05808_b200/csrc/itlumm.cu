@@ -19,8 +19,7 @@
 #include "encode.cuh"
 #include "simt.cuh"
 #include "tc.cuh"
-#include "sp.cuh"
-#include "tc2.cuh"
+#include "tcp.cuh"
 
 using namespace itlumm;
 
@@ -62,15 +61,15 @@ struct itlumm_plan_s {
   SimtCfg simt{};
   TcPlan tc{};
   TcPlan tcs{};                  // the same tiling with the 2:4-sparse one-hot (f2)
-  itlumm_onehot onehot = ITLUMM_ONEHOT_DENSE;
+  itlumm_onehot onehot = ITLUMM_ONEHOT_AUTO;
+  TcpPlan pair_sp{};             // CTA-pair kernel over the sparse tiling (streamed LUT), AUTO's choice
+  TcpPlan pair_dn{};             // the same over the dense tiling
   // TC_PIPE code scratch (allocated at plan creation; reuse ordered by scratch_ev)
   std::mutex scratch_mu;
   uint8_t* scratch = nullptr;
   int64_t scratch_rows = 0, scratch_ldc = 0;
   cudaEvent_t scratch_ev = nullptr;
   bool scratch_used = false;
-  uint32_t* ready = nullptr;     // [scratch_rows / 128] x 2: TC_SP ready / consumed counters (zeroed)
-  bool coop = false;             // device supports cooperative launches
   double seg_frac[2] = {1.0, 1.0};  // fraction of a row's 64-byte segments the gather touches (f32, bf16)
   bool packed = false;           // split-packed input: gather column of (c, t) is 4c + t
   // host API staging
@@ -290,7 +289,6 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   auto cleanup = [&](itlumm_status st) {
     if (P->dmem) cudaFree(P->dmem);
     if (P->scratch) cudaFree(P->scratch);
-    if (P->ready) cudaFree(P->ready);
     if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
     delete P;
     cudaSetDevice(prev);
@@ -335,21 +333,14 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
     P->tcs.trace = P->tc.trace;
   }
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
+  if (P->tcs.ok && P->tcs.stream_b) tcp_configure(P->pair_sp, P->tcs, P->num_sms);
+  if (P->tc.ok && P->tc.stream_b) tcp_configure(P->pair_dn, P->tc, P->num_sms);
+  P->pair_sp.trace = P->pair_dn.trace = P->tc.trace;
   if (P->tc.ok || P->tcs.ok) {
     P->scratch_ldc = (((C + 1) / 2) + 15) & ~15;
     P->scratch_rows = 262144;
     e = cudaMalloc(&P->scratch, (size_t)P->scratch_rows * P->scratch_ldc);
     if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "scratch cudaMalloc: %s", cudaGetErrorString(e)));
-    e = cudaMalloc(&P->ready, (size_t)P->scratch_rows / 128 * 2 * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMemset(P->ready, 0, (size_t)P->scratch_rows / 128 * 2 * sizeof(uint32_t));
-    if (e != cudaSuccess) return cleanup(fail(ITLUMM_ENOMEM, "ready counters: %s", cudaGetErrorString(e)));
-    int coop = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cuda_device);
-    P->coop = coop != 0;
-    cudaFuncSetAttribute((const void*)k_amm_sp<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    cudaFuncSetAttribute((const void*)k_amm_sp<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-    cudaFuncSetAttribute((const void*)k_amm_sp<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     e = cudaEventCreateWithFlags(&P->scratch_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cleanup(fail(ITLUMM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
   }
@@ -371,7 +362,6 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
   cudaDeviceSynchronize();
   if (P->dmem) cudaFree(P->dmem);
   if (P->scratch) cudaFree(P->scratch);
-  if (P->ready) cudaFree(P->ready);
   if (P->tc.trace) cudaFree(P->tc.trace);
   if (P->scratch_ev) cudaEventDestroy(P->scratch_ev);
   if (P->stage) cudaFree(P->stage);
@@ -386,8 +376,7 @@ extern "C" itlumm_status itlumm_plan_destroy(itlumm_plan P) {
 extern "C" itlumm_status itlumm_plan_set_algo(itlumm_plan P, itlumm_algo algo) {
   g_err.clear();
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
-  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC && algo != ITLUMM_ALGO_TC_PIPE &&
-      algo != ITLUMM_ALGO_TC_SP)
+  if (algo != ITLUMM_ALGO_AUTO && algo != ITLUMM_ALGO_SIMT && algo != ITLUMM_ALGO_TC && algo != ITLUMM_ALGO_TC_PIPE)
     return fail(ITLUMM_EINVAL, "bad algo %d", (int)algo);
   P->algo = algo;
   return ITLUMM_OK;
@@ -406,7 +395,8 @@ extern "C" itlumm_status itlumm_plan_set_summation(itlumm_plan P, itlumm_summati
 extern "C" itlumm_status itlumm_plan_set_onehot(itlumm_plan P, itlumm_onehot o) {
   g_err.clear();
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
-  if (o != ITLUMM_ONEHOT_DENSE && o != ITLUMM_ONEHOT_SPARSE24) return fail(ITLUMM_EINVAL, "bad onehot %d", (int)o);
+  if (o != ITLUMM_ONEHOT_AUTO && o != ITLUMM_ONEHOT_DENSE && o != ITLUMM_ONEHOT_SPARSE24)
+    return fail(ITLUMM_EINVAL, "bad onehot %d", (int)o);
   if (o == ITLUMM_ONEHOT_SPARSE24 && !P->tcs.ok)
     return fail(ITLUMM_EUNSUPPORTED, "2:4-sparse one-hot tiling unsupported for this plan: %s", P->tcs.why);
   P->onehot = o;
@@ -438,8 +428,21 @@ static itlumm_status check_A(itlumm_plan P, const void* A, itlumm_dtype dtype, i
   if (N < 0) return fail(ITLUMM_EINVAL, "N < 0");
   if (dtype != ITLUMM_F32 && dtype != ITLUMM_BF16) return fail(ITLUMM_EINVAL, "bad dtype %d", (int)dtype);
   if (N > 0 && !A) return fail(ITLUMM_EINVAL, "A is NULL");
-  if (lda < P->D) return fail(ITLUMM_EINVAL, "lda (%lld) < D (%d)", (long long)lda, P->D);
+  if (lda < P->D) return fail(ITLUMM_ESHAPE, "lda (%lld) < D (%d)", (long long)lda, P->D);
   return ITLUMM_OK;
+}
+
+// A device pointer the caller passes must be device (or managed) memory of the plan's device.
+static itlumm_status check_dev(itlumm_plan P, const void* ptr, const char* what) {
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ITLUMM_EINVAL, "%s: not a CUDA-visible pointer (%s)", what, cudaGetErrorString(e));
+  }
+  if (at.type == cudaMemoryTypeManaged || (at.type == cudaMemoryTypeDevice && at.device == P->device)) return ITLUMM_OK;
+  return fail(ITLUMM_EINVAL, "%s is not device memory of the plan's device %d (memory type %d, device %d)", what,
+              P->device, (int)at.type, at.device);
 }
 
 // Rows per stage R and ring depth S of the streaming encoder for rows of rb bytes, or false if
@@ -553,19 +556,36 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
   g_launches = 0;
   itlumm_status st = check_A(P, A, dtype, lda, N);
   if (st != ITLUMM_OK) return st;
-  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_EINVAL, "ldc (%lld) < ceil(C/2) (%d)", (long long)ldc, (P->C + 1) / 2);
+  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_ESHAPE, "ldc (%lld) < ceil(C/2) (%d)", (long long)ldc, (P->C + 1) / 2);
   if (N == 0) return ITLUMM_OK;
   if (!codes) return fail(ITLUMM_EINVAL, "codes is NULL");
+  if ((st = check_dev(P, A, "A")) != ITLUMM_OK || (st = check_dev(P, codes, "codes")) != ITLUMM_OK) return st;
   DeviceGuard dg(P->device);
   return launch_encode(P, A, dtype, lda, N, codes, ldc, (cudaStream_t)stream);
 }
 
-// The tensor-core tiling in use: dense or 2:4-sparse one-hot.
+// The 1-CTA tensor-core tiling in use: dense (AUTO, DENSE) or 2:4-sparse one-hot (SPARSE24).
 static const TcPlan& tcp(itlumm_plan P) { return P->onehot == ITLUMM_ONEHOT_SPARSE24 ? P->tcs : P->tc; }
+
+// Tensor-core accumulate of codes (a3' + a4).  A streamed LUT runs on the CTA-pair kernel (dense
+// one-hot unless SPARSE24 is asked for), everything else on the 1-CTA k_tc.
+// Developer knob (not ABI): ITLUMM_PAIR=0 keeps streamed LUTs on k_tc.
+static itlumm_status launch_tc_acc(itlumm_plan P, const TcArgs& a, cudaStream_t s, bool pdl) {
+  static const bool pair_on = !(getenv("ITLUMM_PAIR") && atoi(getenv("ITLUMM_PAIR")) == 0);
+  const TcPlan& t = tcp(P);
+  if (pair_on && t.ok && t.stream_b) {
+    const TcpPlan& pp = P->onehot == ITLUMM_ONEHOT_SPARSE24 ? P->pair_sp : P->pair_dn;
+    if (pp.ok) {
+      const itlumm_status st = tcp_launch(pp, P->dp, a, s, pdl);
+      if (st != ITLUMM_EUNSUPPORTED) return st;
+    }
+  }
+  return tc_launch(t, P->dp, false, false, a, s, pdl);
+}
 
 static bool use_tc(itlumm_plan P) {
   if (P->algo == ITLUMM_ALGO_SIMT || P->summation != ITLUMM_SUM_EXACT) return false;
-  if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
+  if (P->algo == ITLUMM_ALGO_TC || P->algo == ITLUMM_ALGO_TC_PIPE) return true;
   return tc_preferred(tcp(P), P->simt.MS != 0);
 }
 
@@ -574,7 +594,7 @@ static bool use_tc(itlumm_plan P) {
 // and the tree walks once per M slice).
 static bool use_pipe(itlumm_plan P) {
   if (!tcp(P).ok || P->summation != ITLUMM_SUM_EXACT) return false;
-  if (P->algo == ITLUMM_ALGO_TC_PIPE || P->algo == ITLUMM_ALGO_TC_SP) return true;
+  if (P->algo == ITLUMM_ALGO_TC_PIPE) return true;
   // AUTO pipes every tensor-core shape through the streaming encoder: a streamed LUT has no fused
   // TC kernel, with several slices a fused kernel would repeat the gather per slice, and even with
   // one slice the fused kernel's per-thread gather is latency-bound (cfg1: 10.0 us fused vs 6.6 us
@@ -591,12 +611,15 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
     TcArgs a{};
     a.A = A; a.lda = lda; a.codes = codes; a.ldc = ldc; a.N = N; a.acc = acc; a.ldacc = ldacc;
     a.out = out; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
-    bool launched = false;
-    itlumm_status st = (fused || t.sp) ? ITLUMM_OK : tc2_launch(t, P->dp, a, s, P->num_sms, false, &launched);
-    if (st == ITLUMM_OK && !launched) st = tc_launch(t, P->dp, fused, dtype == ITLUMM_BF16, a, s);
-    if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
-    g_launches = 1;
-    return ITLUMM_OK;
+    itlumm_status st = fused ? tc_launch(t, P->dp, true, dtype == ITLUMM_BF16, a, s) : launch_tc_acc(P, a, s, false);
+    if (st == ITLUMM_OK) {
+      g_launches = 1;
+      return ITLUMM_OK;
+    }
+    // AUTO never fails on a shape the CUDA-core kernels take (e.g. a streamed LUT with codes rows
+    // that are not 16-byte multiples): fall through to SIMT; an explicit TC request reports the error
+    if (!(st == ITLUMM_EUNSUPPORTED && P->algo == ITLUMM_ALGO_AUTO && P->simt.MS != 0))
+      return fail(st, "%s", tc_last_msg());
   }
   const SimtCfg& c = P->simt;
   if (c.MS == 0) return fail(ITLUMM_EUNSUPPORTED, "SIMT LUT kernel: C = %d too large for a resident LUT slice", P->C);
@@ -648,104 +671,9 @@ static itlumm_status launch_pipe(itlumm_plan P, const void* A, itlumm_dtype dtyp
     TcArgs a{};
     a.codes = P->scratch; a.ldc = P->scratch_ldc; a.N = rows;
     a.out = out + (size_t)r0 * ldo; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
-    bool launched = false;
-    const TcPlan& t = tcp(P);
-    if (!t.sp) st = tc2_launch(t, P->dp, a, s, P->num_sms, true, &launched);
-    if (st == ITLUMM_OK && !launched) st = tc_launch(t, P->dp, false, false, a, s, true);
+    st = launch_tc_acc(P, a, s, true);
     if (st != ITLUMM_OK) return fail(st, "%s", tc_last_msg());
     launches += 2;
-  }
-  if (!capturing) {
-    CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
-    P->scratch_used = true;
-  }
-  g_launches = launches;
-  return ITLUMM_OK;
-}
-
-// TC_SP: one cooperative launch; E encoder CTAs + T = n*G tensor-core CTAs (see sp.cuh).
-// Returns EUNSUPPORTED (without launching) where the rows cannot be bulk-copied or the
-// cooperative grid does not fit; the caller then falls back to TC_PIPE.
-static itlumm_status launch_sp(itlumm_plan P, const void* A, itlumm_dtype dtype, int64_t lda, int64_t N,
-                               float* out, int64_t ldo, itlumm_epilogue epi, cudaStream_t s) {
-  const int es = dtype == ITLUMM_BF16 ? 2 : 4;
-  const int64_t rb = (int64_t)P->D * es;
-  const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * es) % 16 == 0) && (rb % 16 == 0);
-  const int enc_warps = kTcThreads / 32 - 1;
-  const TcPlan& t = P->tc;
-  if (P->onehot != ITLUMM_ONEHOT_DENSE) return fail(ITLUMM_EUNSUPPORTED, "TC_SP runs the dense one-hot only");
-  // split: encoder share ~ bytes read / (bytes read + 1.25 x bytes written) (developer override:
-  // ITLUMM_SP_ENC_CTAS)
-  static const int enc_override = getenv("ITLUMM_SP_ENC_CTAS") ? atoi(getenv("ITLUMM_SP_ENC_CTAS")) : 0;
-  const double rd = (double)P->D * es, wr = 1.25 * 4.0 * P->M;
-  int E = enc_override > 0 ? enc_override : (int)(P->num_sms * rd / (rd + wr) + 0.5);
-  int T = (P->num_sms - E) / t.G * t.G;
-  if (T < t.G) T = t.G;
-  E = P->num_sms - T;
-  if (E < 1) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: too few SMs for the split");
-  // fewer encoder SMs each keep proportionally more bytes in flight (same total as the
-  // standalone encoder), with up to 16 stages (the TC role's shared memory is there anyway)
-  static const int sp_infl = getenv("ITLUMM_SP_INFLIGHT_KB") ? atoi(getenv("ITLUMM_SP_INFLIGHT_KB")) : 0;
-  const int infl_kb = sp_infl > 0 ? sp_infl : (int)std::min<int64_t>(190, 100LL * P->num_sms / E);
-  int R = 0, S = 0;
-  if (!P->coop || !aligned || !enc_tiling(P, rb, enc_warps, true, &R, &S, infl_kb, 16))
-    return fail(ITLUMM_EUNSUPPORTED, "TC_SP needs cooperative launch and 16-byte aligned rows");
-  int CS = 0;
-  size_t smem_tc = 0;
-  for (int cs = 4; cs >= 1; --cs) {
-    smem_tc = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)P->scratch_ldc, t.stream_b, false, t.ST).total;
-    if (smem_tc <= kSmemMax) { CS = cs; break; }
-  }
-  const size_t smem = std::max(smem_tc, enc_smem_bytes(P->C, R, S, (int)rb));
-  if (CS == 0 || smem > kSmemMax) return fail(ITLUMM_EUNSUPPORTED, "TC_SP: shared memory budget exceeded");
-  std::lock_guard<std::mutex> lk(P->scratch_mu);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CUDA_TRY(cudaStreamIsCapturing(s, &cap));
-  const bool capturing = cap != cudaStreamCaptureStatusNone;
-  if (P->scratch_used && !capturing) CUDA_TRY(cudaStreamWaitEvent(s, P->scratch_ev, 0));
-  int32_t launches = 0;
-  for (int64_t r0 = 0; r0 < N; r0 += P->scratch_rows) {
-    const int64_t rows = std::min<int64_t>(P->scratch_rows, N - r0);
-    EncArgs ge{};
-    ge.A = (const uint8_t*)A + (size_t)r0 * lda * es; ge.lda = lda; ge.N = rows;
-    ge.codes = P->scratch; ge.ldc = P->scratch_ldc;
-    ge.R = R; ge.S = S; ge.row_bytes = (int)rb; ge.contiguous = lda == P->D; ge.pdl = 0;
-    ge.packed = P->packed ? 1 : 0;
-    ge.fixed_ok = 1;
-    TcKArgs gt{};
-    gt.codes = P->scratch; gt.ldc = P->scratch_ldc; gt.N = rows;
-    gt.out = out + (size_t)r0 * ldo; gt.ldo = ldo; gt.relu = epi == ITLUMM_EPI_RELU;
-    gt.qt = t.qt; gt.KB = t.KB; gt.NS = t.NS; gt.G = t.G; gt.tmem_cols = t.tmem_cols;
-    gt.CS = CS; gt.pdl = 0;
-    gt.ready = P->ready; gt.consumed = P->ready + P->scratch_rows / 128;
-    gt.enc_R = R; gt.enc_warps = enc_warps;
-    gt.stream_b = t.stream_b ? 1 : 0;
-    gt.ST = t.ST;
-    gt.trace = t.trace;
-    alignas(64) CUtensorMap out_map;
-    memset(&out_map, 0, sizeof out_map);
-    gt.tma_store = make_out_map(&out_map, gt.out, rows, P->M, ldo) ? 1 : 0;
-    SpArgs sp{E};
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(E + T));
-    cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e;
-    if (t.stream_b)
-      e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t, true>, P->dp, ge, gt, sp, out_map)
-                               : cudaLaunchKernelEx(&cfg, k_amm_sp<float, true>, P->dp, ge, gt, sp, out_map);
-    else
-      e = dtype == ITLUMM_BF16 ? cudaLaunchKernelEx(&cfg, k_amm_sp<uint16_t, false>, P->dp, ge, gt, sp, out_map)
-                               : cudaLaunchKernelEx(&cfg, k_amm_sp<float, false>, P->dp, ge, gt, sp, out_map);
-    if (e == cudaSuccess) e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(ITLUMM_ECUDA, "k_amm_sp launch: %s", cudaGetErrorString(e));
-    ++launches;
   }
   if (!capturing) {
     CUDA_TRY(cudaEventRecord(P->scratch_ev, s));
@@ -763,12 +691,16 @@ extern "C" itlumm_status itlumm_lut_accumulate(itlumm_plan P, const uint8_t* cod
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
   if (N < 0) return fail(ITLUMM_EINVAL, "N < 0");
   if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
-  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_EINVAL, "ldc (%lld) < ceil(C/2)", (long long)ldc);
-  if (acc && ldacc < P->M) return fail(ITLUMM_EINVAL, "ldacc < M");
-  if (out && ldo < P->M) return fail(ITLUMM_EINVAL, "ldo < M");
+  if (ldc < (P->C + 1) / 2) return fail(ITLUMM_ESHAPE, "ldc (%lld) < ceil(C/2)", (long long)ldc);
+  if (acc && ldacc < P->M) return fail(ITLUMM_ESHAPE, "ldacc < M");
+  if (out && ldo < P->M) return fail(ITLUMM_ESHAPE, "ldo < M");
   if (N == 0) return ITLUMM_OK;
   if (!codes) return fail(ITLUMM_EINVAL, "codes is NULL");
   if (!acc && !out) return fail(ITLUMM_EINVAL, "acc and out are both NULL");
+  itlumm_status st;
+  if ((st = check_dev(P, codes, "codes")) != ITLUMM_OK) return st;
+  if (acc && (st = check_dev(P, acc, "acc")) != ITLUMM_OK) return st;
+  if (out && (st = check_dev(P, out, "out")) != ITLUMM_OK) return st;
   DeviceGuard dg(P->device);
   return launch_lut(P, false, nullptr, ITLUMM_F32, 0, codes, ldc, N, acc, ldacc, out, ldo, epi, (cudaStream_t)stream);
 }
@@ -780,18 +712,12 @@ extern "C" itlumm_status itlumm_amm(itlumm_plan P, const void* A, itlumm_dtype d
   itlumm_status st = check_A(P, A, dtype, lda, N);
   if (st != ITLUMM_OK) return st;
   if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
-  if (ldo < P->M) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
+  if (ldo < P->M) return fail(ITLUMM_ESHAPE, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
   if (N == 0) return ITLUMM_OK;
   if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  if ((st = check_dev(P, A, "A")) != ITLUMM_OK || (st = check_dev(P, out, "out")) != ITLUMM_OK) return st;
   DeviceGuard dg(P->device);
-  if (use_pipe(P)) {
-    if (P->algo == ITLUMM_ALGO_TC_SP) {
-      st = launch_sp(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
-      if (st != ITLUMM_EUNSUPPORTED) return st;
-      g_err.clear();
-    }
-    return launch_pipe(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
-  }
+  if (use_pipe(P)) return launch_pipe(P, A, dtype, lda, N, out, ldo, epi, (cudaStream_t)stream);
   return launch_lut(P, true, A, dtype, lda, nullptr, 0, N, nullptr, 0, out, ldo, epi, (cudaStream_t)stream);
 }
 
@@ -803,7 +729,7 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
   itlumm_status st = check_A(P, A_host, dtype, lda, N);
   if (st != ITLUMM_OK) return st;
   if (epi != ITLUMM_EPI_NONE && epi != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue");
-  if (ldo < P->M) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
+  if (ldo < P->M) return fail(ITLUMM_ESHAPE, "ldo (%lld) < M (%d)", (long long)ldo, P->M);
   if (N == 0) return ITLUMM_OK;
   if (!out_host) return fail(ITLUMM_EINVAL, "out_host is NULL");
   std::lock_guard<std::mutex> lk(P->host_mu);
@@ -839,9 +765,7 @@ extern "C" itlumm_status itlumm_amm_host(itlumm_plan P, const void* A_host, itlu
     else
       CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, hA, (size_t)lda * es, row_in, rows, cudaMemcpyHostToDevice, s));
     if (use_pipe(P)) {
-      st = ITLUMM_EUNSUPPORTED;
-      if (P->algo == ITLUMM_ALGO_TC_SP) st = launch_sp(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
-      if (st == ITLUMM_EUNSUPPORTED) { g_err.clear(); st = launch_pipe(P, dA, dtype, P->D, rows, dO, P->M, epi, s); }
+      st = launch_pipe(P, dA, dtype, P->D, rows, dO, P->M, epi, s);
     } else {
       st = launch_lut(P, true, dA, dtype, P->D, nullptr, 0, rows, nullptr, 0, dO, P->M, epi, s);
     }
@@ -891,7 +815,7 @@ extern "C" itlumm_status itlumm_mlp_create(const itlumm_params* layers, const it
   if (!layers || !epis || n_layers < 1) return fail(ITLUMM_EINVAL, "layers/epis NULL or n_layers < 1");
   for (int l = 0; l + 1 < n_layers; ++l)
     if (layers[l + 1].D != layers[l].M)
-      return fail(ITLUMM_EINVAL, "layer %d has D = %d but layer %d has M = %d", l + 1, layers[l + 1].D, l, layers[l].M);
+      return fail(ITLUMM_ESHAPE, "layer %d has D = %d but layer %d has M = %d", l + 1, layers[l + 1].D, l, layers[l].M);
   for (int l = 0; l < n_layers; ++l)
     if (epis[l] != ITLUMM_EPI_NONE && epis[l] != ITLUMM_EPI_RELU) return fail(ITLUMM_EINVAL, "bad epilogue of layer %d", l);
   // columns of layer l's output that layer l+1 splits on (sorted, distinct)
@@ -966,9 +890,10 @@ extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_
   const int L = (int)m->plans.size();
   itlumm_status st = check_A(m->plans[0], A, dtype, lda, N);
   if (st != ITLUMM_OK) return st;
-  if (ldo < m->width[L - 1]) return fail(ITLUMM_EINVAL, "ldo (%lld) < M (%d)", (long long)ldo, m->width[L - 1]);
+  if (ldo < m->width[L - 1]) return fail(ITLUMM_ESHAPE, "ldo (%lld) < M (%d)", (long long)ldo, m->width[L - 1]);
   if (N == 0) return ITLUMM_OK;
   if (!out) return fail(ITLUMM_EINVAL, "out is NULL");
+  if ((st = check_dev(m->plans[0], A, "A")) != ITLUMM_OK || (st = check_dev(m->plans[0], out, "out")) != ITLUMM_OK) return st;
   DeviceGuard dg(m->device);
   const int64_t rows_max = std::min<int64_t>(m->chunk, N);
   if (m->buf_rows < rows_max) {

@@ -79,18 +79,11 @@ struct TcKArgs {
   int CS;          // codes ring stages; > 0 selects the bulk-copy (TMA) codes path
   int pdl;         // launched as a programmatic dependent of the encode kernel
   int tma_store;   // out written by TMA tensor stores through out_map (else per-thread stores)
-  // spatial pipeline (k_amm_sp): codes tile t may be loaded once ready[t] reaches
-  // ceil(rows(t) / enc_R) (one count per published encode tile); the last of the
-  // G slice CTAs to observe it resets ready[t] and consumed[t] for the next call.
-  uint32_t* ready;
-  uint32_t* consumed;
-  int enc_R, enc_warps;
   // streamed-B mode (LUT larger than shared memory, codes path only): work items are
   // (row tile, slice) pairs u = cta + k * ncta, slice = u / ntiles (consecutive CTAs share a slice,
   // so its K-blocks stream from L2); each stage carries the one-hot K-block and the LUT K-block.
   int stream_b;
   int ST;          // ring stages
-  int BST;         // k_tc2: LUT-half ring stages
   int out_hint;    // L2 policy of the output tensor stores (l2_policy kind; 0 = default)
   uint64_t* trace; // developer timeline (ITLUMM_TC_TRACE): [8 CTAs][4 roles][kTraceEv] globaltimer stamps
 };
@@ -395,8 +388,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
 
   if (warp == kTcLoaderWarp) {
     // ============================================================== codes loader (one lane)
-    // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring; in the
-    // spatial pipeline each tile is first awaited on its ready counter.
+    // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring.
     if (!FUSED && CS > 0 && lane == 0) {
       int cs = 0, stage = 0;
       uint32_t cph = 0, phase = 0;
@@ -406,21 +398,6 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         mbar_wait(codes_empty + cs, cph ^ 1);
         const int64_t r0 = tile * kTcRows;
         const int rows = (int)((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows);
-        if (g.ready) {
-          const uint32_t need = (uint32_t)((rows + g.enc_R - 1) / g.enc_R);
-          spin_until_geq(g.ready + tile, need);
-          asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
-          // items reading this tile: one per slice, `parts` for leftover (split) units
-          uint32_t nread = 0;
-          for (int s2 = 0; s2 < G; ++s2) {
-            const int64_t u2 = SB ? (int64_t)s2 * ntiles + tile : tile;
-            nread += (u2 >= full * nworkers) ? (uint32_t)parts : 1u;
-          }
-          if (atomicAdd(g.consumed + tile, 1u) == nread - 1) {   // last reader to look
-            g.ready[tile] = 0u;
-            g.consumed[tile] = 0u;
-          }
-        }
         const uint32_t bytes = (uint32_t)(rows * g.ldc);
         mbar_arrive_expect_tx(codes_bar + cs, bytes);
         bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
@@ -457,12 +434,16 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         mbar_wait(codes_bar + cs, cph);
         const bool valid = tile * kTcRows + r < g.N;
         const uint8_t* crow = codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
+        uint4 quad = make_uint4(0, 0, 0, 0);
         for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t cw = valid ? *reinterpret_cast<const uint32_t*>(crow + kb * 4) : 0u;
+          // one 16-byte read per 4 K-blocks: a 4-byte read per K-block of rows ldc apart was a
+          // 32-way bank conflict when ldc is a multiple of 128 (cfg5; ncu r02)
+          if ((kb & 3) == 0 && valid) quad = *reinterpret_cast<const uint4*>(crow + kb * 4);
+          const uint32_t cw = (kb & 3) == 0 ? quad.x : (kb & 3) == 1 ? quad.y : (kb & 3) == 2 ? quad.z : quad.w;
           uint32_t code[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) code[j] = (valid && kb * 8 + j < C) ? (cw >> (4 * j)) & 15u : 16u;
-          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
+          mbar_wait_sleep(empty_bar + stage, phase ^ 1, 32);   // MMA finished reading this stage
           put_onehot<SP>(a_s + (size_t)stage * kAStage, r, code);
           fence_proxy_async_smem();
           mbar_arrive(full_bar + stage);
@@ -558,7 +539,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     // One thread, kept lean: the tensor core only stays busy if the issuing thread turns a K-block
     // around in less than its MMA time (272 ns at N=256); descriptors are precomputed and advanced
     // by adding to the start-address field (addr >> 4; shared addresses < 256 KB never carry).
-    if (lane == 0) {
+    {
+      // the whole warp runs the loop (warp-uniform values stay in uniform registers), one elected
+      // lane issues each tcgen05 op (a lone lane == 0 thread wrapped every op in an elect loop and
+      // moved every descriptor through R2UR: ~190 ns per stage in the k_tcp timeline, profiles/r02)
       const uint32_t idesc = idesc_i8(NS);
       if (!SB) mbar_wait(b_bar, 0);                  // resident LUT slice in shared memory
       const uint32_t a0 = smem_u32(a_s);
@@ -573,8 +557,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait(acce_bar + acc, acc_phase ^ 1);    // epilogue drained this accumulator
-        stamp(1);
+        mbar_wait_sleep(acce_bar + acc, acc_phase ^ 1, 32);   // epilogue drained this accumulator
+        if (lane == 0) stamp(1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
         for (int kb = 0; kb < KB; ++kb) {
@@ -582,22 +566,25 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           tc_fence_after();
           const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((SB ? stage : kb) * b_step);
-          if (SP) {
-            // metadata rows -> TMEM columns 2NS + 4*stage (in tcgen05 issue order before the MMAs
-            // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each; A +32 B, B +64 B)
-            const uint32_t e = tmem_base + (uint32_t)(2 * NS + 4 * stage);
-            tmem_cp_128x128b(e, m_desc0 + (uint64_t)(stage * a_step));
-            umma_sp_i8(d, ad, bd, e, idesc, kb != 0);
-            umma_sp_i8(d, ad + 2, bd + 4, e + 2, idesc, 1u);
-          } else {
-            umma_i8(d, ad, bd, idesc, kb != 0);          // K = 32 per MMA: +32 B on both operands
-            umma_i8(d, ad + 2, bd + 2, idesc, 1u);
-            umma_i8(d, ad + 4, bd + 4, idesc, 1u);
-            umma_i8(d, ad + 6, bd + 6, idesc, 1u);
+          if (elect_one()) {
+            if (SP) {
+              // metadata rows -> TMEM columns 2NS + 4*stage (in tcgen05 issue order before the MMAs
+              // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each; A +32 B, B +64 B)
+              const uint32_t e = tmem_base + (uint32_t)(2 * NS + 4 * stage);
+              tmem_cp_128x128b(e, m_desc0 + (uint64_t)(stage * a_step));
+              umma_sp_i8(d, ad, bd, e, idesc, kb != 0);
+              umma_sp_i8(d, ad + 2, bd + 4, e + 2, idesc, 1u);
+            } else {
+              umma_i8(d, ad, bd, idesc, kb != 0);          // K = 32 per MMA: +32 B on both operands
+              umma_i8(d, ad + 2, bd + 2, idesc, 1u);
+              umma_i8(d, ad + 4, bd + 4, idesc, 1u);
+              umma_i8(d, ad + 6, bd + 6, idesc, 1u);
+            }
+            umma_commit(empty_bar + stage);             // frees the stage when these MMAs finish
+            if (kb == KB - 1) umma_commit(accf_bar + acc);
           }
-          umma_commit(empty_bar + stage);             // frees the stage when these MMAs finish
-          stamp(1);
-          if (kb == KB - 1) umma_commit(accf_bar + acc);
+          __syncwarp();
+          if (lane == 0) stamp(1);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -626,7 +613,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       int sl, c0, c1;
       const uint64_t opol = l2_policy(g.out_hint);
       for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
-        mbar_wait(accf_bar + acc, acc_phase);
+        mbar_wait_sleep(accf_bar + acc, acc_phase, 128);
         tc_fence_after();
         if (warp == kTcEpiWarp0 && lane == 0) stamp(2);
         const int m0 = sl * NS;
@@ -646,10 +633,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
                                  : *reinterpret_cast<const float4*>(scp + j0 + 4 * c);
             const float4 o4 = SB ? __ldg(reinterpret_cast<const float4*>(otp + j0 + 4 * c))
                                  : *reinterpret_cast<const float4*>(otp + j0 + 4 * c);
-            y[4 * c + 0] = fmaf(s4.x, __uint2float_rn(v[4 * c + 0]), o4.x);   // a4, one rounding (R8)
-            y[4 * c + 1] = fmaf(s4.y, __uint2float_rn(v[4 * c + 1]), o4.y);
-            y[4 * c + 2] = fmaf(s4.z, __uint2float_rn(v[4 * c + 2]), o4.z);
-            y[4 * c + 3] = fmaf(s4.w, __uint2float_rn(v[4 * c + 3]), o4.w);
+            y[4 * c + 0] = fmaf(s4.x, u2f_exact(v[4 * c + 0]), o4.x);   // a4, one rounding (R8)
+            y[4 * c + 1] = fmaf(s4.y, u2f_exact(v[4 * c + 1]), o4.y);
+            y[4 * c + 2] = fmaf(s4.z, u2f_exact(v[4 * c + 2]), o4.z);
+            y[4 * c + 3] = fmaf(s4.w, u2f_exact(v[4 * c + 3]), o4.w);
           }
           if (g.relu) {
 #pragma unroll
@@ -689,7 +676,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     int64_t tile;
     int sl, c0, c1;
     for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
-      mbar_wait(accf_bar + acc, acc_phase);
+      mbar_wait_sleep(accf_bar + acc, acc_phase, 128);
       tc_fence_after();
       const int m0 = sl * NS;
       if (sl != cur_sl) {                             // this lane's scale/offtot, per slice
@@ -738,10 +725,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           for (int it = 0; it < 8; ++it) {
             const int rr = it * 4 + rsub;
             const uint4 a4 = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
-            float y0 = fmaf(scv[i][0], __uint2float_rn(a4.x), otv[i][0]);
-            float y1 = fmaf(scv[i][1], __uint2float_rn(a4.y), otv[i][1]);
-            float y2 = fmaf(scv[i][2], __uint2float_rn(a4.z), otv[i][2]);
-            float y3 = fmaf(scv[i][3], __uint2float_rn(a4.w), otv[i][3]);
+            float y0 = fmaf(scv[i][0], u2f_exact(a4.x), otv[i][0]);
+            float y1 = fmaf(scv[i][1], u2f_exact(a4.y), otv[i][1]);
+            float y2 = fmaf(scv[i][2], u2f_exact(a4.z), otv[i][2]);
+            float y3 = fmaf(scv[i][3], u2f_exact(a4.w), otv[i][3]);
             if (g.relu) { y0 = relu_pos0(y0); y1 = relu_pos0(y1); y2 = relu_pos0(y2); y3 = relu_pos0(y3); }
             __stcs(reinterpret_cast<float4*>(o), make_float4(y0, y1, y2, y3));
             o += step;
@@ -754,10 +741,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           const int rr = it * 4 + rsub;
           const int64_t grow = row0 + rr;
           const uint4 a4 = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((cq ^ (rr & 7)) << 4));
-          float y0 = fmaf(scv[i][0], __uint2float_rn(a4.x), otv[i][0]);
-          float y1 = fmaf(scv[i][1], __uint2float_rn(a4.y), otv[i][1]);
-          float y2 = fmaf(scv[i][2], __uint2float_rn(a4.z), otv[i][2]);
-          float y3 = fmaf(scv[i][3], __uint2float_rn(a4.w), otv[i][3]);
+          float y0 = fmaf(scv[i][0], u2f_exact(a4.x), otv[i][0]);
+          float y1 = fmaf(scv[i][1], u2f_exact(a4.y), otv[i][1]);
+          float y2 = fmaf(scv[i][2], u2f_exact(a4.z), otv[i][2]);
+          float y3 = fmaf(scv[i][3], u2f_exact(a4.w), otv[i][3]);
           if (g.relu) { y0 = relu_pos0(y0); y1 = relu_pos0(y1); y2 = relu_pos0(y2); y3 = relu_pos0(y3); }
           if (grow < g.N) {
             float* o = g.out + grow * g.ldo + mcol;
@@ -804,6 +791,7 @@ inline const char* tc_last_msg() { return g_tc_msg; }
 inline void tc_layout_host(int C, int M, const uint8_t* lut, TcPlan* t, std::vector<uint8_t>& qt, bool sparse = false) {
   qt.clear();
   t->C = C; t->M = M;
+  if (255LL * C >= (1LL << 23)) { t->ok = false; t->why = "C too large for the exact 2^23 float conversion"; return; }
   t->sp = sparse;
   const int ns_hw = sparse ? kSpNsMax : 256;     // TMEM: 2 accumulators (+ sparse metadata) <= 512 columns
   t->KB = (16 * C + kKBlock - 1) / kKBlock;

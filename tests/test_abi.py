@@ -29,7 +29,7 @@ def test_exports_every_header_symbol(lib):
     assert set(syms) == set(_lib.EXPORTS), syms
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.itlumm_abi_version() == 4
+    assert lib.itlumm_abi_version() == 5
 
 
 def test_sm100a_only_binary():
@@ -113,4 +113,4 @@ def test_header_is_plain_c_and_links(tmp_path):
                         f"-Wl,-rpath,{lib_dir}", "-o", exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True)
-    assert r.returncode == 0 and r.stdout.startswith("ok 4"), (r.returncode, r.stdout, r.stderr)
+    assert r.returncode == 0 and r.stdout.startswith("ok 5"), (r.returncode, r.stdout, r.stderr)

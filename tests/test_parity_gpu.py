@@ -15,17 +15,28 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = ATOL = 1e-6
-# "_sp24": the same schedule with the 2:4-sparse one-hot operand (tcgen05.mma.sp)
-ALGOS = ["simt", "tc", "tc_pipe", "tc_sp", "tc_sp24", "tc_pipe_sp24"]
+# "_sp24" / "_dense": the same schedule with the one-hot operand forced to the 2:4-sparse form
+# (tcgen05.mma.sp) or the dense form; plain names use the library's choice (AUTO: sparse
+# on the CTA-pair streamed-LUT kernel, dense on the 1-CTA kernel)
+ALGOS = ["auto", "simt", "tc", "tc_pipe", "tc_sp24", "tc_pipe_sp24", "tc_pipe_dense"]
 
 
 def _set(plan, algo):
-    if algo.endswith("_sp24"):
-        plan.set_algo(algo[:-5])
-        plan.set_onehot("sparse24")
-    else:
-        plan.set_algo(algo)
-        plan.set_onehot("dense")
+    for suffix, onehot in (("_sp24", "sparse24"), ("_dense", "dense")):
+        if algo.endswith(suffix):
+            plan.set_algo(algo[: -len(suffix)])
+            plan.set_onehot(onehot)
+            return
+    plan.set_algo(algo)
+    plan.set_onehot("auto")
+
+
+def _skip_or_raise(algo, e):
+    """Only an explicitly requested tensor-core schedule may refuse a shape (its documented
+    EUNSUPPORTED, e.g. the fused TC kernel on a streamed LUT); AUTO and SIMT must run everything."""
+    if algo.startswith("tc") and e.status == 3:
+        pytest.skip(f"{algo} unsupported for this shape: {e}")
+    raise e
 
 
 def _plan(params, algo):
@@ -65,19 +76,29 @@ def run_all(params, A, relu, dtype, algo):
     assert np.array_equal(unpack(codes.cpu().numpy(), params["C"]), ref["codes"])
     if params["C"] % 2:
         assert np.all(codes.cpu().numpy()[:, -1] >> 4 == 0)     # R14 padding nibble
+    _set(plan, algo)
+    # the fused call and the two-step call are checked independently: a schedule that refuses one
+    # of them must not hide the other
+    skipped = []
     try:
-        _set(plan, algo)
+        y = plan.amm(Ad, relu=relu)
+        torch.cuda.synchronize()
+        assert_out(y.cpu().numpy(), ref["y"])
+    except ItlummError as e:
+        skipped.append(e)
+    try:
         acc = torch.empty((A.shape[0], params["M"]), dtype=torch.int32, device="cuda")
         out, _ = plan.lut_accumulate(codes, acc=acc, relu=relu)
-        y = plan.amm(Ad, relu=relu)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref["acc"])
+        assert_out(out.cpu().numpy(), ref["y"])
+        out2, _ = plan.lut_accumulate(codes, relu=relu)          # fp32 only (the TMA-store epilogue)
+        torch.cuda.synchronize()
+        assert_out(out2.cpu().numpy(), ref["y"])
     except ItlummError as e:
-        if algo.startswith("tc") and e.status == 3:
-            pytest.skip(f"tc path unsupported for this shape: {e}")
-        raise
-    torch.cuda.synchronize()
-    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref["acc"])
-    assert_out(out.cpu().numpy(), ref["y"])
-    assert_out(y.cpu().numpy(), ref["y"])
+        skipped.append(e)
+    if skipped:
+        _skip_or_raise(algo, skipped[0])
     return plan, ref
 
 
@@ -128,9 +149,7 @@ def test_parity_cfg2_full_sampled(algo):
         y = plan.amm(Ad, relu=True)
         y2, _ = plan.lut_accumulate(codes, relu=True)
     except ItlummError as e:
-        if algo.startswith("tc") and e.status == 3:
-            pytest.skip(str(e))
-        raise
+        _skip_or_raise(algo, e)
     torch.cuda.synchronize()
     y, y2, codes = y.cpu().numpy(), y2.cpu().numpy(), codes.cpu().numpy()
     assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
@@ -168,9 +187,7 @@ def test_edge_strides_alignment_and_specials(algo):
         plan.amm(Ad, out=mis, relu=True)
         empty = plan.amm(Ad[:0], relu=True)
     except ItlummError as e:
-        if algo.startswith("tc") and e.status == 3:
-            pytest.skip(str(e))
-        raise
+        _skip_or_raise(algo, e)
     torch.cuda.synchronize()
     assert_out(big[:, :48].cpu().numpy(), ref["y"])
     assert np.all(big[:, 48:].cpu().numpy() == -7.0)
@@ -199,12 +216,34 @@ def test_error_paths_on_device():
     params = ofit.fit(w["A_train"], w["B"], 4, w["perm"], w["bias"])
     plan = Plan(params)
     A = torch.from_numpy(w["A"]).cuda()
-    with pytest.raises(ItlummError):
-        plan.amm(A[:, :30].contiguous())             # lda < D
+    # the binding rejects what raw pointers cannot show: width, dtype, device, strides
+    with pytest.raises(ValueError):
+        plan.amm(A[:, :30].contiguous())             # fewer than D columns
     with pytest.raises(TypeError):
         plan.amm(A.double())
-    with pytest.raises(ItlummError):
-        plan.amm(A, out=torch.empty((10, 4), device="cuda"))   # ldo < M
+    with pytest.raises(ValueError):
+        plan.amm(A, out=torch.empty((10, 4), device="cuda"))   # fewer than M columns
+    with pytest.raises(ValueError):
+        plan.amm(A.cpu())                            # host rows to a device call
+    with pytest.raises(ValueError):
+        plan.amm(A.t().contiguous().t())             # column-major rows
+    with pytest.raises(TypeError):
+        plan.lut_accumulate(plan.encode(A), acc=torch.empty((10, 8), dtype=torch.int64, device="cuda"))
+    # the C ABI itself: strides inconsistent with the plan are ESHAPE, host pointers are EINVAL
+    import ctypes
+    from paper_2207_05808_b200 import _lib
+    lib = _lib.load()
+    out = torch.empty((10, 8), device="cuda")
+    st = lib.itlumm_amm(plan._h, ctypes.c_void_p(A.data_ptr()), _lib.F32, 30, 10,
+                        ctypes.c_void_p(out.data_ptr()), 8, 0, None)
+    assert st == _lib.ESHAPE and "lda" in lib.itlumm_last_error().decode()
+    st = lib.itlumm_amm(plan._h, ctypes.c_void_p(A.data_ptr()), _lib.F32, 40, 10,
+                        ctypes.c_void_p(out.data_ptr()), 4, 0, None)
+    assert st == _lib.ESHAPE
+    Ah = A.cpu()
+    st = lib.itlumm_amm(plan._h, ctypes.c_void_p(Ah.data_ptr()), _lib.F32, 40, 10,
+                        ctypes.c_void_p(out.data_ptr()), 8, 0, None)
+    assert st == _lib.EINVAL and "device memory" in lib.itlumm_last_error().decode()
 
 
 def _mlp_case(C, n_rows, n_train, layers):
@@ -236,7 +275,7 @@ def test_mlp_chain_small(C, layers):
     assert_out(y.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("C", [16, 64])
+@pytest.mark.parametrize("C", [16, 64, 128, 256])
 def test_mlp_cfg4_shapes_sampled(C):
     """BASELINE configs[3] layer shapes 3072-1024-1024-10 (N = 70000 rows: two 65536-row seed
     chunks, ragged tail), sampled rows against the oracle's full-layer chain."""
@@ -246,7 +285,7 @@ def test_mlp_cfg4_shapes_sampled(C):
     y = mlp.forward(torch.from_numpy(w["A"]).cuda())
     torch.cuda.synchronize()
     y = y.cpu().numpy()
-    rows = np.unique(np.concatenate([np.random.default_rng(1).choice(70000, 600, replace=False), [0, 69999]]))
+    rows = sample_rows(70000, 1200, seed=1)
     ref = oracle.mlp_forward(oparams, w["relus"], w["A"][rows])
     assert_out(y[rows], ref)
 
@@ -277,28 +316,85 @@ def test_parity_avg16(seed, N, D, M, C, dtype):
     assert_out(ye.cpu().numpy(), oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, nthreads=8)["y"])
 
 
-def test_parity_cta_pair_kernel_streamed_lut(monkeypatch):
-    """The cta_group::2 pair kernel (k_tc2, opt-in ITLUMM_TC2=1) on streamed LUTs: bit-exact vs the
-    oracle (run in a subprocess so the opt-in flag is read at library load)."""
+def test_parity_one_cta_streamed_lut_kernel():
+    """ITLUMM_PAIR=0 keeps streamed LUTs on the 1-CTA k_tc (developer knob, read at library load):
+    that schedule stays bit-exact vs the oracle on the small streamed cases and on cfg3 C=128 at full
+    size (several slices, full work rounds)."""
+    import os
     import subprocess
     import sys
     code = (
         "import numpy as np, torch, synth, oracle\n"
         "from oracle import fit as ofit\n"
         "from paper_2207_05808_b200 import Plan\n"
-        "for seed, N, D, M, C, dt in [(10, 3000, 4096, 512, 256, 'bf16'), (14, 700, 2048, 300, 512, 'f32')]:\n"
+        "from tests.test_parity_gpu import sample_rows\n"
+        "for seed, N, D, M, C, dt in [(9, 4097, 256, 256, 64, 'bf16'), (10, 3000, 4096, 512, 256, 'bf16'), (14, 700, 2048, 300, 512, 'f32')]:\n"
         "    w = synth.small_case(seed, N=N, D=D, M=M, C=C, dtype=dt, n_train=600)\n"
         "    p = ofit.fit(w['A_train'], w['B'], C, w['perm'], w['bias'], a_is_bf16=dt == 'bf16')\n"
         "    ref = oracle.amm(p, w['A'], relu=w['relu'], dtype=dt, nthreads=8)['y']\n"
         "    A = torch.from_numpy(w['A'].view(np.int16) if dt == 'bf16' else w['A']).cuda()\n"
         "    A = A.view(torch.bfloat16) if dt == 'bf16' else A\n"
-        "    y = Plan(p).amm(A, relu=w['relu']).cpu().numpy()\n"
-        "    assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), seed\n"
+        "    for oh in ('dense', 'sparse24'):\n"
+        "        pl = Plan(p); pl.set_onehot(oh)\n"
+        "        y = pl.amm(A, relu=w['relu']).cpu().numpy()\n"
+        "        assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), (seed, oh)\n"
+        "w = synth.workload('cfg3_c128')\n"
+        "p = ofit.fit(w['A_train'], w['B'], w['C'], w['perm'], w['bias'])\n"
+        "y = Plan(p).amm(torch.from_numpy(w['A']).cuda()).cpu().numpy()\n"
+        "rows = sample_rows(w['A'].shape[0], 2048, seed=5)\n"
+        "ref = oracle.amm(p, w['A'][rows], relu=False, nthreads=8)['y']\n"
+        "assert np.array_equal(y[rows].view(np.uint32), ref.view(np.uint32))\n"
         "print('ok')\n")
-    import os
-    env = dict(os.environ, ITLUMM_TC2="1", PYTHONPATH=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ITLUMM_PAIR="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def sample_rows(N: int, n: int, seed: int = 0) -> np.ndarray:
+    """At least n distinct rows of an N-row call: the first and last rows, both sides of every
+    128-row (1-CTA tile) and 256-row (CTA-pair tile) boundary among the first and last 8 tiles and
+    among 32 random tiles, the 262144-row scratch-chunk edges, and random rows."""
+    g = np.random.default_rng(seed)
+    picks = [0, 1, 2, N - 3, N - 2, N - 1]
+    ntile = (N + 127) // 128
+    tiles = set(range(min(8, ntile))) | set(range(max(0, ntile - 8), ntile))
+    tiles |= set(g.choice(ntile, min(32, ntile), replace=False).tolist())
+    for t in tiles:
+        for d in (-1, 0, 1, 127):
+            picks.append(t * 128 + d)
+    for e in range(262144, N + 1, 262144):
+        picks += [e - 1, e]
+    rows = np.unique(np.clip(np.array(picks), 0, N - 1))
+    if len(rows) < n:
+        rest = np.setdiff1d(np.arange(N), rows)
+        rows = np.unique(np.concatenate([rows, g.choice(rest, min(n - len(rows), len(rest)), replace=False)]))
+    return rows
+
+
+@pytest.mark.parametrize("name,onehot", [("cfg3_c64", "auto"), ("cfg3_c64", "sparse24"), ("cfg3_c128", "auto"),
+                                         ("cfg3_c128", "sparse24"), ("cfg5", "auto")])
+def test_benched_streamed_lut_shapes_full_size_sampled(name, onehot):
+    """BASELINE configs[2] (C = 64, 128) and configs[4] at FULL size in the launch configuration
+    bench.py times (AUTO: encode -> CTA-pair tensor-core accumulate over a streamed LUT with several
+    slices and many full work rounds): >= 4096 sampled rows, chosen across tile and slice-row
+    boundaries, bit-exact vs the oracle; every row finite."""
+    from paper_2207_05808_b200 import Plan
+    w = synth.workload(name)
+    dtype = w["dtype"]
+    params = ofit.fit(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=dtype == "bf16")
+    plan = Plan(params)
+    plan.set_onehot(onehot)
+    N = w["A"].shape[0]
+    y = plan.amm(_dev(w["A"], dtype), relu=w["relu"])
+    torch.cuda.synchronize()
+    assert plan.last_launch_count == 2 * ((N + 262143) // 262144)    # encode + accumulate per chunk
+    y = y.cpu().numpy()
+    rows = sample_rows(N, 4096, seed=3)
+    assert len(rows) >= 4096
+    ref = oracle.amm(params, w["A"][rows], relu=w["relu"], dtype=dtype, nthreads=16)["y"]
+    assert_out(y[rows], ref)
+    assert np.all(np.isfinite(y))
 
 
 def test_eq3_lut_optimisation_gpu_vs_oracle():

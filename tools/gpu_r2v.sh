@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out/r2v
+timeout 300 python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "parity_small and (9-4097 or 10-3000 or 14-700 or 5-2049)" > gpurun_out/r2v/pytest.log 2>&1
+for d in 0 2048 1; do echo "dbg=$d" >> gpurun_out/r2v/kb.txt; ITLUMM_TCP_DBG=$d timeout 300 python tools/kbench.py --workload cfg5 --algos tc,tc_dense --only acc --iters 10 >> gpurun_out/r2v/kb.txt 2>&1; done
+ITLUMM_PAIR=0 timeout 300 python tools/kbench.py --workload cfg5 --algos tc --only acc --iters 10 >> gpurun_out/r2v/kb.txt 2>&1
+timeout 300 python tools/tcp_trace.py cfg5 tc_dense > gpurun_out/r2v/trace_d.txt 2>&1
+timeout 300 python tools/tcp_trace.py cfg5 tc > gpurun_out/r2v/trace_s.txt 2>&1

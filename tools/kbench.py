@@ -91,12 +91,12 @@ def main():
         res["encode_ms"] = timeit(lambda: plan.encode(A, codes=codes), args.iters)
     for algo in args.algos.split(","):
         try:
-            if algo.endswith("_sp24"):          # same schedule, 2:4-sparse one-hot operand
-                plan.set_algo(algo[:-5])
-                plan.set_onehot("sparse24")
-            else:
-                plan.set_algo(algo)
-                plan.set_onehot("dense")
+            base, onehot = algo, "auto"
+            for suffix, oh in (("_sp24", "sparse24"), ("_dense", "dense")):
+                if algo.endswith(suffix):
+                    base, onehot = algo[: -len(suffix)], oh
+            plan.set_algo(base)
+            plan.set_onehot(onehot)
             if "acc" in only:
                 res[f"{algo}_accumulate_ms"] = timeit(lambda: plan.lut_accumulate(codes, out=out, relu=cfg["relu"]), args.iters)
             if "fused" not in only:

@@ -23,7 +23,7 @@ for seed, N, D, M, C, dt in [(2, 333, 97, 33, 10, "f32"), (3, 300, 96, 40, 12, "
     A = torch.from_numpy(w["A"].view(np.int16) if dt == "bf16" else w["A"]).cuda()
     if dt == "bf16":
         A = A.view(torch.bfloat16)
-    for algo in ("simt", "tc", "tc_pipe", "tc_sp"):
+    for algo in ("simt", "tc", "tc_pipe"):
         plan = Plan(p, algo=algo)
         try:
             y = plan.amm(A, relu=True).cpu().numpy()
