@@ -4,9 +4,11 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--algo auto|simt|tc]
   python bench.py --impl reference ...     # the CPU oracle, timed as it stands (reference arm)
 
+Default workload: cfg5 (BASELINE configs[4], the largest single-GPU single-layer config).
 N > 1 runs under torchrun (one process per GPU, NCCL): rank 0 fits the layer once and
-broadcasts its parameters; every rank then processes its own N rows (weak scaling, no
-collective in the data path).  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
+broadcasts its parameters (one packed payload); the config's fixed global row count is sharded
+over the ranks (strong scaling; --scaling weak gives every rank the full N instead), with no
+collective in the data path.  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
 """
 from __future__ import annotations
 
@@ -93,15 +95,19 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def i8_peak():
-    """Dense int8 tensor peak for the one-hot x LUT contraction: the measured bf16 GEMM burst
-    (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio 2 (4.5 / 2.25 PFLOP/s dense)."""
+def i8_peaks():
+    """Two dense int8 peaks for the one-hot x LUT contraction: the measured bf16 GEMM burst
+    (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio 2 (4.5 / 2.25 PFLOP/s dense), and the
+    kind::i8 issue rate measured by the builder's probe (tools/probes/mma_rate.cu:
+    profiles/r01/mma_rate.jsonl, 4558 dense-equivalent TOPS at N=256)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return 2.0 * float(d["bf16_tflops"]), "measured bf16 burst (MEASURED_PEAKS.json) x 2 (int8/bf16 nominal ratio)"
-    return 2.0 * 1590.0, "fallback (B200_PROFILING.md: 1.59 PF bf16) x 2"
+        bf = (2.0 * float(d["bf16_tflops"]), "measured bf16 burst (MEASURED_PEAKS.json) x 2 (int8/bf16 nominal ratio)")
+    else:
+        bf = (2.0 * 1590.0, "fallback (B200_PROFILING.md: 1.59 PF bf16) x 2")
+    return [bf, (4558.0, "measured tcgen05 kind::i8 issue rate (profiles/r01/mma_rate.jsonl, N=256)")]
 
 
 def alg_bytes(w: dict, n: int) -> int:
@@ -110,15 +116,16 @@ def alg_bytes(w: dict, n: int) -> int:
     return n * (4 * w["C"] * s_a + 4 * w["M"]) + 16 * w["C"] * w["M"]
 
 
-def ncu_traffic(workload: str, algo: str):
-    """dram read+write bytes per launch from the committed ncu --set full summary, or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def ncu_traffic(workload: str, algo: str, n_gpus: int, rows: int):
+    """DRAM read+write bytes of one call from a committed ncu capture of that exact step (the
+    capture's command line, rows and n_gpus are recorded next to the number), or None."""
+    p = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    v = d.get(f"{workload}:{algo}")
-    return v if isinstance(v, (int, float)) else None
+    v = d.get(f"{workload}:{algo}:rows={rows}")
+    return v if isinstance(v, dict) else None
 
 
 class ClockSampler:
@@ -189,7 +196,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     base, packed = base_workload(args.workload)
     cfg = synth.CONFIGS[base]
-    n = cfg["N"] if args.rows is None else args.rows
+    n_global = (cfg["N"] if args.rows is None else args.rows) * (world if args.scaling == "weak" else 1)
+    # strong scaling: the fixed global row count split over the ranks; weak: every
+    # rank its own full N rows of the seeded stream
+    r0, r1 = pdist.shard_rows(n_global, world, rank)
+    n = r1 - r0
     relu = cfg["relu"]
     bf16 = cfg["dtype"] == "bf16"
 
@@ -199,15 +210,14 @@ def run_ours(args):
         w0 = synth.workload(base, n_rows=0)
         params = fit_layer(w0["A_train"], w0["B"], w0["C"], w0["perm"], w0["bias"], a_is_bf16=bf16)
     if world > 1:
-        params = pdist.broadcast_params(params, dev)
+        params = pdist.broadcast_params(params, dev)          # one packed payload over NCCL
     cols = None
     if packed:
         params, cols = _split_packed(params)
     plan = Plan(params, device=local, algo=args.algo)
 
-    # this rank's rows (weak scaling: rank r owns rows [r*n, (r+1)*n) of the seeded stream)
-    r0, r1 = pdist.weak_rows(n, rank)
-    A_host = synth.rows(cfg["dist"], cfg["cfg"], 0, r0, r1, cfg["D"])
+    # this rank's rows [r0, r1) of the seeded stream (chunk-seeded: the same rows for any world size)
+    A_host = gen_rows(cfg["dist"], cfg["cfg"], 0, r0, r1, cfg["D"])
     if packed:
         A_host = np.ascontiguousarray(A_host[:, cols])
     A_t = torch.from_numpy(A_host.view(np.int16) if bf16 else A_host)
@@ -272,7 +282,7 @@ def run_ours(args):
         total_ms = pdist.max_over_ranks(total_ms, dev)
     ms_per_step = total_ms / args.steps
     launch_ms = ms_per_step                      # one itlumm_amm call per step
-    rows_per_s = n * world / (ms_per_step * 1e-3)
+    rows_per_s = n_global / (ms_per_step * 1e-3)
     del g_steps
 
     # per-kernel breakdown of the step (same plan, same buffers, graph-timed through the C ABI)
@@ -299,13 +309,14 @@ def run_ours(args):
         ]
         del g_enc, g_acc
         # the accumulate's other roofline (SURVEY 8(d) "tensor int8 ceiling = peak / (32 C M)"):
-        # the one-hot x LUT product is 2 * 16C * M int8 ops per row
-        pk, pk_src = i8_peak()
+        # the one-hot x LUT product is 2 * 16C * M int8 ops per row (16x the method's C*M
+        # lookup-adds: it describes the tensor-core formulation, not the method's work)
         ops = 32.0 * cfg["C"] * cfg["M"] * n
-        kernels[1]["tensor"] = {"bound": "tensor", "achieved": ops / (t_acc * 1e-3) / 1e12, "peak": pk,
-                                "unit": "TOPS (int8, dense-equivalent one-hot MMA work)",
-                                "frac": ops / (t_acc * 1e-3) / 1e12 / pk, "peak_source": pk_src,
-                                "ops_per_launch": ops}
+        ach = ops / (t_acc * 1e-3) / 1e12
+        kernels[1]["tensor"] = [{"bound": "tensor", "achieved": ach, "peak": pk,
+                                 "unit": "TOPS (int8, dense-equivalent one-hot MMA work)",
+                                 "frac": ach / pk, "peak_source": src, "ops_per_launch": ops}
+                                for pk, src in i8_peaks()]
 
     # end to end through the host-buffer C-ABI call (H2D + kernel + D2H inside the region)
     out_pin = torch.empty((n, cfg["M"]), dtype=torch.float32).pin_memory()
@@ -323,7 +334,7 @@ def run_ours(args):
     if world > 1:
         e2e_s = pdist.max_over_ranks(e2e_s, dev)
         dist.barrier()
-    e2e = {"value": n * world / e2e_s, "unit": "rows/s",
+    e2e = {"value": n_global / e2e_s, "unit": "rows/s",
            "h2d_bytes_per_step": int(A_host.nbytes), "d2h_bytes_per_step": int(n * cfg["M"] * 4),
            "api": "itlumm_amm_host (pinned host buffers, chunked H2D/kernel/D2H)", "steps": k_e2e}
 
@@ -338,39 +349,37 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": rows_per_s, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded stand-in for the dataset, DESIGN.md input recipe)",
             "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
-                       "rows_per_gpu": n, "global_rows": n * world, "D": int(params["D"]), "C": cfg["C"],
+                       "rows_per_gpu": n, "global_rows": n_global, "D": int(params["D"]), "C": cfg["C"],
                        "M": cfg["M"], "input": ("bf16" if bf16 else "f32") + (" split-packed" if packed else " row-major"),
                        "epilogue": "relu" if relu else "none", "algo": args.algo,
-                       "parallelism": f"rows sharded dp{world}",
+                       "parallelism": f"rows sharded dp{world}" + (" (strong: fixed global N)" if args.scaling == "strong"
+                                                                   else " (weak: N rows per rank)"),
                        "l2": f"inputs larger than L2: A {A_host.nbytes / 2**20:.0f} MiB per step, {nbuf} rotating "
                              f"A/out buffer sets ({nbuf * A_host.nbytes / 2**20:.0f} MiB of A between reuses of a buffer)",
                        "timing": "K steps captured as one CUDA graph, replayed once between CUDA events",
                        "compute": "uint8 LUT, exact int32 accumulate, fp32 compare + fmaf dequant"},
             "output_elems_per_s": rows_per_s * cfg["M"],
+            # the method's bytes (A split columns + output + LUT) of one itlumm_amm call
+            # over its device time, against the measured HBM copy bandwidth
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload, args.algo),
+                         "frac": achieved / peak,
+                         "traffic": (tr["bytes"] if (tr := ncu_traffic(args.workload, args.algo, world, n)) else None),
+                         "traffic_source": (tr["source"] if tr else "no committed ncu capture of this step"),
                          "alg_bytes_per_launch": ab, "launch_ms": launch_ms,
                          "peak_source": peak_src,
                          "kernel": f"itlumm_amm ({per_step_launches} kernel launch(es) per call)",
                          "kernels": kernels},
-            # when the tensor-core accumulate dominates the call and sits closer to its int8 roofline
-            # than the call to HBM (streamed-LUT shapes), that is the roofline that binds
+            # secondary: the tensor-core accumulate against the int8 roofline of its one-hot x LUT
+            # formulation (16x the method's work), both peaks
             "roofline_tensor": (kernels[1]["tensor"] if kernels else None),
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
-        if kernels and kernels[1]["ms"] > kernels[0]["ms"] and kernels[1]["tensor"]["frac"] > line["roofline"]["frac"]:
-            hbm = line["roofline"]
-            tr = dict(kernels[1]["tensor"])
-            tr.update(kernel="k_tc (dominant kernel of the call: one-hot x LUT on tcgen05 + dequant)",
-                      launch_ms=kernels[1]["ms"], traffic=None, kernels=kernels)
-            line["roofline"] = tr
-            line["roofline_hbm"] = {k: v for k, v in hbm.items() if k != "kernels"}
     plan.close()
     if world > 1:
         dist.destroy_process_group()
@@ -392,16 +401,17 @@ def run_ours_mlp(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     C = int(args.workload.split("_c")[1])
-    n = synth.MLP_CFG["N"] if args.rows is None else args.rows
+    n_global = (synth.MLP_CFG["N"] if args.rows is None else args.rows) * (world if args.scaling == "weak" else 1)
+    r0, r1 = pdist.shard_rows(n_global, world, rank)
+    n = r1 - r0
     layers = synth.MLP_LAYERS
     w = synth.mlp_workload(C, 0)
     params = None
     if rank == 0:
         params = fit_mlp(w["A_train"], w["Bs"], w["Cs"], w["perms"], w["biases"], w["relus"], device=local)
     if world > 1:
-        params = [pdist.broadcast_params(params[l] if rank == 0 else None, dev) for l in range(len(layers))]
+        params = pdist.broadcast_layers(params, dev)          # every layer in one packed payload
     mlp = Mlp(params, w["relus"], device=local)
-    r0, r1 = pdist.weak_rows(n, rank)
     A_host = gen_rows(synth.MLP_CFG["dist"], synth.MLP_CFG["cfg"], 0, r0, r1, layers[0][0])
     A_pin = torch.from_numpy(A_host).pin_memory()
     nbuf = 2
@@ -448,25 +458,28 @@ def run_ours_mlp(args):
         total_ms = pdist.max_over_ranks(total_ms, dev)
     del g
     ms_per_step = total_ms / args.steps
-    rows_per_s = n * world / (ms_per_step * 1e-3)
-    # end to end through the public API: pinned H2D of the rows, forward, D2H of the logits
+    rows_per_s = n_global / (ms_per_step * 1e-3)
+    # end to end through the public host-buffer C-ABI call (itlumm_mlp_forward_host: pinned H2D of
+    # the rows, forward, D2H of the logits, pipelined in chunks inside the library)
     out_pin = torch.empty((n, M), dtype=torch.float32).pin_memory()
-    k_e2e = max(3, min(args.steps, args.e2e_steps))
-    A_e = torch.empty_like(A_dev[0])
-    o_e = torch.empty_like(out_dev[0])
+    k_e2e = max(2, min(args.steps, args.e2e_steps))
+    mlp.forward_host(A_pin, out=out_pin)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(k_e2e):
-        A_e.copy_(A_pin, non_blocking=True)
-        mlp.forward(A_e, out=o_e)
-        out_pin.copy_(o_e, non_blocking=True)
+        mlp.forward_host(A_pin, out=out_pin)
     torch.cuda.synchronize(dev)
     e2e_s = (time.perf_counter() - t0) / k_e2e
     if world > 1:
         e2e_s = pdist.max_over_ranks(e2e_s, dev)
     widths = mlp.widths()
-    ab_row = sum(4 * C * 4 + 4 * m for (_, m, _) in layers)
-    ab = n * ab_row + sum(16 * C * m for (_, m, _) in layers)
+    # bytes the method moves with dead-column elimination: layer l reads its 4C split columns and
+    # writes the widths[l] columns it computes (the last layer all M), plus its LUT of those columns
+    ab_row = sum(4 * C * 4 + 4 * wl for wl in widths)
+    ab = n * ab_row + sum(16 * C * wl for wl in widths)
+    ab_full = n * sum(4 * C * 4 + 4 * m for (_, m, _) in layers) + sum(16 * C * m for (_, m, _) in layers)
     peak, peak_src = peaks()
     achieved = ab / (ms_per_step * 1e-3) / 1e9
     line = None
@@ -484,10 +497,10 @@ def run_ours_mlp(args):
         line = {
             "metric": METRIC, "value": rows_per_s, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded stand-in for CIFAR-shaped rows, DESIGN.md input recipe)",
             "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
-                       "rows_per_gpu": n, "global_rows": n * world, "layers": layers, "C": C,
+                       "rows_per_gpu": n, "global_rows": n_global, "layers": layers, "C": C,
                        "computed_widths": widths, "input": "f32 row-major",
                        "parallelism": f"rows sharded dp{world}",
                        "l2": f"inputs larger than L2 (A {A_host.nbytes / 2**30:.1f} GiB/step), {nbuf} rotating buffers",
@@ -496,10 +509,13 @@ def run_ours_mlp(args):
                          "frac": achieved / peak, "traffic": None,
                          "alg_bytes_per_launch": ab, "launch_ms": ms_per_step, "peak_source": peak_src,
                          "kernel": f"itlumm_mlp_forward ({launches // args.steps} launches per call)",
-                         "note": "algorithmic bytes of the three full layers (SURVEY 8(d): 48C + 8232 B/row); "
-                                 "hidden layers compute only the columns the next layer splits on"},
-            "e2e": {"value": n * world / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": int(A_host.nbytes),
-                    "d2h_bytes_per_step": int(n * M * 4), "api": "torch pinned copies + Mlp.forward",
+                         "note": "bytes the method moves with dead-column elimination (each layer: its 4C split "
+                                 "columns in, the columns it computes out, their LUT); the three full-width "
+                                 "layers would be full_width_alg_bytes",
+                         "full_width_alg_bytes": ab_full},
+            "e2e": {"value": n_global / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": int(A_host.nbytes),
+                    "d2h_bytes_per_step": int(n * M * 4),
+                    "api": "itlumm_mlp_forward_host (pinned host buffers, chunked H2D/forward/D2H)",
                     "steps": k_e2e},
             "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
         }
@@ -568,7 +584,7 @@ def run_reference(args):
     sample = f"first {per_step} of the {n} rows of {args.workload} per step"
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
                        "rows_per_step": per_step, "D": cfg["D"], "C": cfg["C"], "M": cfg["M"]},
@@ -599,7 +615,7 @@ def run_reference_mlp(args):
     v = per_step * args.steps / dt
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD_DESC[args.workload], "name": args.workload,
                        "rows_per_step": per_step, "C": C},
@@ -611,10 +627,12 @@ def run_reference_mlp(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the config's global row count split over the ranks; weak: N rows per rank")
     ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc", "tc_pipe"])
     ap.add_argument("--rows", type=int, default=None, help="override rows per GPU (default: config N)")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -624,6 +642,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1:                      # the driver checks the communicator's rank count here
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         line = run_reference(args)
     elif args.workload.startswith("cfg4"):

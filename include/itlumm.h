@@ -204,6 +204,13 @@ itlumm_status itlumm_mlp_info(itlumm_mlp mlp, int32_t* n_layers, int32_t* widths
 itlumm_status itlumm_mlp_forward(itlumm_mlp mlp, const void* A, itlumm_dtype dtype, int64_t lda,
                                  int64_t N, float* out, int64_t ldo, void* stream);
 
+/* Forward pass on HOST buffers (end-to-end API, as itlumm_amm_host): A_host [N][lda] (dtype),
+ * out_host fp32 [N][ldo].  Rows stream through MLP-owned device staging in ~64 MB chunks; the H2D
+ * of chunk i+1 and the D2H of chunk i-1 overlap the forward of chunk i (forwards run on `stream`).
+ * BLOCKING: returns when out_host is written.  Errors: as itlumm_mlp_forward. */
+itlumm_status itlumm_mlp_forward_host(itlumm_mlp mlp, const void* A_host, itlumm_dtype dtype, int64_t lda,
+                                      int64_t N, float* out_host, int64_t ldo, void* stream);
+
 /* Number of kernel launches the last successful launching call on this thread made. */
 int32_t itlumm_last_launch_count(void);
 

@@ -22,7 +22,7 @@ EXPORTS = [
     "itlumm_plan_create", "itlumm_plan_destroy", "itlumm_plan_set_algo", "itlumm_plan_set_summation",
     "itlumm_plan_set_onehot", "itlumm_plan_info",
     "itlumm_encode", "itlumm_lut_accumulate", "itlumm_amm", "itlumm_amm_host",
-    "itlumm_mlp_create", "itlumm_mlp_destroy", "itlumm_mlp_info", "itlumm_mlp_forward",
+    "itlumm_mlp_create", "itlumm_mlp_destroy", "itlumm_mlp_info", "itlumm_mlp_forward", "itlumm_mlp_forward_host",
     "itlumm_last_launch_count", "itlumm_last_error", "itlumm_abi_version",
 ]
 
@@ -68,6 +68,7 @@ def load():
         "itlumm_mlp_destroy": ([V], S),
         "itlumm_mlp_info": ([V, V, V], S),
         "itlumm_mlp_forward": ([V, V, S, I64, I64, V, I64, V], S),
+        "itlumm_mlp_forward_host": ([V, V, S, I64, I64, V, I64, V], S),
         "itlumm_last_launch_count": ([], I32),
         "itlumm_last_error": ([], ctypes.c_char_p),
         "itlumm_abi_version": ([], I32),

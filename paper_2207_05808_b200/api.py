@@ -226,6 +226,20 @@ class Mlp:
                                                 out.stride(0), _stream(stream, self.device)))
         return out
 
+    def forward_host(self, A, out=None, stream=None):
+        """End-to-end: HOST rows (pinned is fastest) -> HOST logits; blocking, the library pipelines
+        H2D / forward / D2H (itlumm_mlp_forward_host)."""
+        N = A.shape[0]
+        _dtype_code(A)
+        _check(A, "A", _a_dtypes(), 0, self.D)
+        if out is None:
+            out = torch.empty((N, self.M), dtype=torch.float32, pin_memory=A.is_pinned())
+        _check(out, "out", (torch.float32,), N, self.M)
+        _lib.check(self._lib.itlumm_mlp_forward_host(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
+                                                     A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
+                                                     out.stride(0), _stream(stream, self.device)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.itlumm_mlp_destroy(self._h)

@@ -791,6 +791,12 @@ struct itlumm_mlp_s {
   std::vector<int> ld;        // row stride of layer l's intermediate buffer (width rounded up to 4)
   std::vector<float*> buf;    // intermediate buffers, chunk rows each (all but the last layer)
   int64_t chunk = 262144, buf_rows = 0;
+  // host API staging (itlumm_mlp_forward_host): 2 input + 2 output slots, copy streams, events
+  std::mutex host_mu;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev[8] = {};
 };
 
 extern "C" itlumm_status itlumm_mlp_destroy(itlumm_mlp m) {
@@ -801,6 +807,10 @@ extern "C" itlumm_status itlumm_mlp_destroy(itlumm_mlp m) {
   cudaSetDevice(m->device);
   cudaDeviceSynchronize();
   for (auto* b : m->buf) if (b) cudaFree(b);
+  if (m->stage) cudaFree(m->stage);
+  if (m->h2d) cudaStreamDestroy(m->h2d);
+  if (m->d2h) cudaStreamDestroy(m->d2h);
+  for (auto& e : m->ev) if (e) cudaEventDestroy(e);
   for (auto p : m->plans) if (p) itlumm_plan_destroy(p);
   cudaSetDevice(prev);
   delete m;
@@ -928,6 +938,78 @@ extern "C" itlumm_status itlumm_mlp_forward(itlumm_mlp m, const void* A, itlumm_
       in = o; dt = ITLUMM_F32; ld_in = ld_o;
     }
   }
+  g_launches = launches;
+  return ITLUMM_OK;
+}
+
+extern "C" itlumm_status itlumm_mlp_forward_host(itlumm_mlp m, const void* A_host, itlumm_dtype dtype, int64_t lda,
+                                                 int64_t N, float* out_host, int64_t ldo, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!m) return fail(ITLUMM_EINVAL, "mlp is NULL");
+  const int L = (int)m->plans.size();
+  itlumm_status st = check_A(m->plans[0], A_host, dtype, lda, N);
+  if (st != ITLUMM_OK) return st;
+  const int Mo = m->width[L - 1];
+  if (ldo < Mo) return fail(ITLUMM_ESHAPE, "ldo (%lld) < M (%d)", (long long)ldo, Mo);
+  if (N == 0) return ITLUMM_OK;
+  if (!out_host) return fail(ITLUMM_EINVAL, "out_host is NULL");
+  std::lock_guard<std::mutex> lk(m->host_mu);
+  DeviceGuard dg(m->device);
+  const size_t es = dtype == ITLUMM_BF16 ? 2 : 4;
+  const int D = m->plans[0]->D;
+  const size_t row_in = (size_t)D * es, row_out = (size_t)Mo * 4;
+  // chunks of ~64 MB of input (at least 1024 rows) through 2 input and 2 output slots: the H2D of
+  // chunk i+1 and the D2H of chunk i-1 overlap the forward of chunk i (forwards run in order on
+  // `stream`, they share the MLP's intermediate buffers)
+  int64_t chunk = std::max<int64_t>(1024, (int64_t)((64u << 20) / row_in));
+  chunk = std::min<int64_t>(chunk, N);
+  const size_t in_b = ((size_t)chunk * row_in + 255) & ~(size_t)255, out_b = ((size_t)chunk * row_out + 255) & ~(size_t)255;
+  const size_t need = 2 * (in_b + out_b);
+  if (m->stage_bytes < need) {
+    if (m->stage) { cudaDeviceSynchronize(); cudaFree(m->stage); m->stage = nullptr; m->stage_bytes = 0; }
+    if (cudaMalloc(&m->stage, need) != cudaSuccess) return fail(ITLUMM_ENOMEM, "staging cudaMalloc(%zu)", need);
+    m->stage_bytes = need;
+  }
+  if (!m->h2d) CUDA_TRY(cudaStreamCreateWithFlags(&m->h2d, cudaStreamNonBlocking));
+  if (!m->d2h) CUDA_TRY(cudaStreamCreateWithFlags(&m->d2h, cudaStreamNonBlocking));
+  for (auto& e : m->ev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // ev[0..1] input slot loaded, ev[2..3] forward done (input slot free, output ready), ev[4..5]
+  // output slot drained, ev[6] start
+  cudaStream_t sc = (cudaStream_t)stream;
+  CUDA_TRY(cudaEventRecord(m->ev[6], sc));
+  CUDA_TRY(cudaStreamWaitEvent(m->h2d, m->ev[6], 0));
+  CUDA_TRY(cudaStreamWaitEvent(m->d2h, m->ev[6], 0));
+  int32_t launches = 0;
+  for (int64_t r0 = 0, i = 0; r0 < N; r0 += chunk, ++i) {
+    const int64_t rows = std::min<int64_t>(chunk, N - r0);
+    const int s = (int)(i & 1);
+    uint8_t* dA = (uint8_t*)m->stage + s * (in_b + out_b);
+    float* dO = (float*)(dA + in_b);
+    const uint8_t* hA = (const uint8_t*)A_host + (size_t)r0 * lda * es;
+    if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(m->h2d, m->ev[2 + s], 0));    // forward of chunk i-2 read the slot
+    if ((size_t)lda * es == row_in)
+      CUDA_TRY(cudaMemcpyAsync(dA, hA, (size_t)rows * row_in, cudaMemcpyHostToDevice, m->h2d));
+    else
+      CUDA_TRY(cudaMemcpy2DAsync(dA, row_in, hA, (size_t)lda * es, row_in, rows, cudaMemcpyHostToDevice, m->h2d));
+    CUDA_TRY(cudaEventRecord(m->ev[s], m->h2d));
+    CUDA_TRY(cudaStreamWaitEvent(sc, m->ev[s], 0));
+    if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, m->ev[4 + s], 0));        // D2H of chunk i-2 drained the slot
+    st = itlumm_mlp_forward(m, dA, dtype, D, rows, dO, Mo, sc);
+    if (st != ITLUMM_OK) return st;
+    launches += g_launches;
+    CUDA_TRY(cudaEventRecord(m->ev[2 + s], sc));
+    CUDA_TRY(cudaStreamWaitEvent(m->d2h, m->ev[2 + s], 0));
+    if (ldo == Mo)
+      CUDA_TRY(cudaMemcpyAsync(out_host + (size_t)r0 * ldo, dO, (size_t)rows * row_out, cudaMemcpyDeviceToHost, m->d2h));
+    else
+      CUDA_TRY(cudaMemcpy2DAsync(out_host + (size_t)r0 * ldo, (size_t)ldo * 4, dO, row_out, row_out, rows,
+                                 cudaMemcpyDeviceToHost, m->d2h));
+    CUDA_TRY(cudaEventRecord(m->ev[4 + s], m->d2h));
+  }
+  CUDA_TRY(cudaStreamSynchronize(m->d2h));
+  CUDA_TRY(cudaStreamSynchronize(sc));
   g_launches = launches;
   return ITLUMM_OK;
 }

@@ -265,7 +265,6 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
   const int CS = FUSED ? 0 : g.CS;
-  static_assert(!(FUSED && SB), "the streamed-LUT mode has no fused variant");
   const int ST = g.ST;                                // A (and streamed-B) ring depth
   const TcSmem L = tc_smem_layout(C, KB, NS, CS, (int)g.ldc, SB, FUSED, ST, SP);
   constexpr int kAStage = SP ? kSpStage : kTcRows * kKBlock;
@@ -388,21 +387,24 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
 
   if (warp == kTcLoaderWarp) {
     // ============================================================== codes loader (one lane)
-    // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring.
-    if (!FUSED && CS > 0 && lane == 0) {
+    // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring (when the
+    // codes rows can be bulk-copied), and with a streamed LUT (SB) the item's LUT K-blocks.
+    if (lane == 0 && ((!FUSED && CS > 0) || SB)) {
       int cs = 0, stage = 0;
       uint32_t cph = 0, phase = 0;
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait(codes_empty + cs, cph ^ 1);
-        const int64_t r0 = tile * kTcRows;
-        const int rows = (int)((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows);
-        const uint32_t bytes = (uint32_t)(rows * g.ldc);
-        mbar_arrive_expect_tx(codes_bar + cs, bytes);
-        bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
-        stamp(3);
-        if (++cs == CS) { cs = 0; cph ^= 1; }
+        if (!FUSED && CS > 0) {
+          mbar_wait(codes_empty + cs, cph ^ 1);
+          const int64_t r0 = tile * kTcRows;
+          const int rows = (int)((g.N - r0) < kTcRows ? (g.N - r0) : (int64_t)kTcRows);
+          const uint32_t bytes = (uint32_t)(rows * g.ldc);
+          mbar_arrive_expect_tx(codes_bar + cs, bytes);
+          bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, bytes, codes_bar + cs);
+          stamp(3);
+          if (++cs == CS) { cs = 0; cph ^= 1; }
+        }
         if (SB) {                                     // this item's LUT K-blocks, one per stage
           const uint32_t bbytes = (uint32_t)NS * kKBlock;
           const uint8_t* src = g.qt + (size_t)sl * KB * bbytes;
@@ -862,6 +864,8 @@ inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   if (t.sp) {
     if ((st = tc_set_attr<true, float, false, true>(kSmemMax)) != ITLUMM_OK) return st;
     if ((st = tc_set_attr<true, uint16_t, false, true>(kSmemMax)) != ITLUMM_OK) return st;
+    if ((st = tc_set_attr<true, float, true, true>(kSmemMax)) != ITLUMM_OK) return st;
+    if ((st = tc_set_attr<true, uint16_t, true, true>(kSmemMax)) != ITLUMM_OK) return st;
     if ((st = tc_set_attr<false, float, false, true>(kSmemMax)) != ITLUMM_OK) return st;
     if ((st = tc_set_attr<false, float, true, true>(kSmemMax)) != ITLUMM_OK) return st;
     t.grid = t.stream_b ? num_sms : t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
@@ -869,6 +873,8 @@ inline itlumm_status tc_configure(TcPlan& t, int num_sms) {
   }
   if ((st = tc_set_attr<true, float, false>(kSmemMax)) != ITLUMM_OK) return st;
   if ((st = tc_set_attr<true, uint16_t, false>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, float, true>(kSmemMax)) != ITLUMM_OK) return st;
+  if ((st = tc_set_attr<true, uint16_t, true>(kSmemMax)) != ITLUMM_OK) return st;
   if ((st = tc_set_attr<false, float, false>(kSmemMax)) != ITLUMM_OK) return st;
   if ((st = tc_set_attr<false, float, true>(kSmemMax)) != ITLUMM_OK) return st;
   t.grid = t.stream_b ? num_sms : t.G * (num_sms / t.G > 0 ? num_sms / t.G : 1);
@@ -918,11 +924,15 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.trace = t.trace;
   static const int out_hint = getenv("ITLUMM_OUT_HINT") ? atoi(getenv("ITLUMM_OUT_HINT")) : 0;   // developer
   k.out_hint = out_hint;
-  if (t.stream_b && fused) { g_tc_msg = "the LUT is streamed (too large to stay resident): no fused TC kernel"; return ITLUMM_EUNSUPPORTED; }
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
   k.tma_store = (!a.acc && make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) ? 1 : 0;
   size_t smem = t.smem;
+  if (fused && t.stream_b) {
+    // fused over a streamed LUT: the threshold/column tables sit next to the LUT ring
+    smem = tc_smem_layout(t.C, t.KB, t.NS, 0, 0, true, true, t.ST, t.sp).total;
+    if (smem > kSmemMax) { g_tc_msg = "fused kernel over a streamed LUT: shared memory budget exceeded"; return ITLUMM_EUNSUPPORTED; }
+  }
   k.CS = 0;
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
     // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
@@ -934,7 +944,6 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   const int64_t ntiles = (a.N + kTcRows - 1) / kTcRows;
   int64_t grid = t.grid;
   if (grid > (int64_t)t.G * ntiles) grid = (int64_t)t.G * ntiles;
-  if (!fused && k.CS == 0 && t.stream_b) { g_tc_msg = "streamed LUT needs 16-byte aligned codes rows (ldc % 16 == 0)"; return ITLUMM_EUNSUPPORTED; }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kTcThreads);
@@ -947,10 +956,15 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e;
   if (t.sp) {
-    if (fused) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false, true>, dp, k, out_map)
-                        : cudaLaunchKernelEx(&cfg, k_tc<true, float, false, true>, dp, k, out_map);
+    if (fused && t.stream_b) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true, true>, dp, k, out_map)
+                                      : cudaLaunchKernelEx(&cfg, k_tc<true, float, true, true>, dp, k, out_map);
+    else if (fused) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false, true>, dp, k, out_map)
+                             : cudaLaunchKernelEx(&cfg, k_tc<true, float, false, true>, dp, k, out_map);
     else if (t.stream_b) e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true, true>, dp, k, out_map);
     else e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false, true>, dp, k, out_map);
+  } else if (fused && t.stream_b) {
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true>, dp, k, out_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, true>, dp, k, out_map);
   } else if (fused) {
     if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false>, dp, k, out_map);
     else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, false>, dp, k, out_map);

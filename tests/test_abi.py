@@ -103,8 +103,7 @@ def test_no_cpu_fallback_in_product_path():
             assert "import oracle" not in src and "from oracle" not in src, fn
 
 
-def test_header_is_plain_c_and_links(tmp_path):
-    """include/itlumm.h compiles as C99 and the library links from C (no torch, no GPU)."""
+def _build_c_smoke(tmp_path):
     import subprocess
     exe = str(tmp_path / "c_abi_smoke")
     lib_dir = os.path.dirname(_lib.LIB_PATH)
@@ -112,5 +111,20 @@ def test_header_is_plain_c_and_links(tmp_path):
                         os.path.join(ROOT, "tests", "c_abi_smoke.c"), "-L", lib_dir, "-litlumm",
                         f"-Wl,-rpath,{lib_dir}", "-o", exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    r = subprocess.run([exe], capture_output=True, text=True)
+    return exe
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/itlumm.h compiles as C99 and the library links from C (no torch, no GPU needed)."""
+    import subprocess
+    r = subprocess.run([_build_c_smoke(tmp_path)], capture_output=True, text=True)
     assert r.returncode == 0 and r.stdout.startswith("ok 5"), (r.returncode, r.stdout, r.stderr)
+
+
+@pytest.mark.gpu
+def test_c_program_pushes_data_through_a_plan(tmp_path):
+    """From plain C on the GPU: plan_create -> amm_host and a 1-layer mlp_forward_host give the
+    hand-worked outputs in tests/c_abi_smoke.c bit for bit; lda < D is ESHAPE."""
+    import subprocess
+    r = subprocess.run([_build_c_smoke(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "ok 5 gpu", (r.returncode, r.stdout, r.stderr)

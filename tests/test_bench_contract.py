@@ -19,4 +19,4 @@ def test_reference_arm_json_line():
               "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["name"] == "cfg2"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["name"] == "cfg5"
