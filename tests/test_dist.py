@@ -88,3 +88,101 @@ def test_broadcast_params_and_max_gloo_world2():
     ref = fit_layer(w["A_train"], w["B"], 5, w["perm"], w["bias"])
     for name, dt in pdist.PARAM_FIELDS:
         assert res[1][0][name] == np.ascontiguousarray(ref[name], dtype=dt).tobytes(), name
+
+
+def _worker_layers(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        layers = None
+        if rank == 0:
+            w = synth.small_case(32, N=16, D=33, M=7, C=4, n_train=300)
+            p1 = fit_layer(w["A_train"], w["B"], 4, w["perm"], w["bias"])
+            w2 = synth.small_case(33, N=16, D=7, M=3, C=2, n_train=300)
+            p2 = fit_layer(w2["A_train"], w2["B"], 2, w2["perm"], w2["bias"])
+            layers = [p1, p2]
+        got = pdist.broadcast_layers(layers, torch.device("cpu"))
+        q.put((rank, [{k: (np.asarray(v).tobytes() if not isinstance(v, int) else v) for k, v in p.items()}
+                      for p in got]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_layers_one_payload_gloo_world2():
+    """Several layers (an MLP) in one packed payload: identical on both ranks, equal to the fit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_layers, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] and len(res[0]) == 2
+    assert (res[1][0]["D"], res[1][0]["C"], res[1][0]["M"]) == (33, 4, 7)
+    assert (res[1][1]["D"], res[1][1]["C"], res[1][1]["M"]) == (7, 2, 3)
+
+
+def test_pack_params_round_trip_and_single_payload():
+    w = synth.small_case(34, N=16, D=29, M=5, C=3, n_train=200)
+    p = fit_layer(w["A_train"], w["B"], 3, w["perm"], w["bias"])
+    hdr, payload = pdist.pack_params([p])
+    assert hdr.tolist() == [1, 29, 3, 5] and payload.dtype == np.uint8 and payload.size % 4 == 0
+    q = pdist.unpack_params(hdr, payload)[0]
+    for name, dt in pdist.PARAM_FIELDS:
+        assert np.array_equal(np.asarray(p[name], dt), q[name]), name
+
+
+def _worker_shard_gpu(rank, world, port, q, N):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import fit as ofit
+        from paper_2207_05808_b200 import Plan
+        params = None
+        if rank == 0:
+            w = synth.small_case(35, N=16, D=300, M=600, C=64, n_train=800)
+            params = ofit.fit(w["A_train"], w["B"], 64, w["perm"], w["bias"])
+        params = pdist.broadcast_params(params, torch.device("cpu"))
+        r0, r1 = pdist.shard_rows(N, world, rank)
+        A = synth.rows("mnist", 135, 0, r0, r1, 300)              # the rank's rows of the seeded stream
+        y = Plan(params, device=0).amm(torch.from_numpy(A).cuda(), relu=True)
+        torch.cuda.synchronize()
+        q.put((rank, y.cpu().numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_row_sharded_ranks_equal_single_gpu_and_oracle():
+    """World size 2 on one GPU (gloo for the broadcast; the ranks' kernels never wait on each
+    other): each rank runs its contiguous shard of a fixed N through Plan.amm (a streamed-LUT,
+    several-slice shape).  The concatenated shard outputs equal the single-process output and the
+    oracle bit for bit (row-parallel bit identity)."""
+    import oracle
+    from oracle import fit as ofit
+    from paper_2207_05808_b200 import Plan
+    N = 5001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_shard_gpu, args=(r, 2, port, q, N)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    ys = np.concatenate([np.frombuffer(res[r], np.float32).reshape(-1, 600) for r in range(2)])
+    w = synth.small_case(35, N=16, D=300, M=600, C=64, n_train=800)
+    params = ofit.fit(w["A_train"], w["B"], 64, w["perm"], w["bias"])
+    A = synth.rows("mnist", 135, 0, 0, N, 300)
+    y1 = Plan(params, device=0).amm(torch.from_numpy(A).cuda(), relu=True).cpu().numpy()
+    ref = oracle.amm(params, A, relu=True, nthreads=8)["y"]
+    assert ys.shape == (N, 600)
+    assert np.array_equal(ys.view(np.uint32), y1.view(np.uint32))
+    assert np.array_equal(ys.view(np.uint32), ref.view(np.uint32))
