@@ -184,6 +184,52 @@ def eq3_objective(A, B, bias, codes, T, T0, lam, relu: bool) -> float:
     return float(((Y - Z) ** 2).sum() + lam * ((np.asarray(T) - np.asarray(T0)) ** 2).sum())
 
 
+def softmax_rows(Z: np.ndarray) -> np.ndarray:
+    """Row-wise softmax, fp64, max-shifted ("a row-wise nonlinearity ... such as softmax")."""
+    Z = np.asarray(Z, np.float64)
+    E = np.exp(Z - Z.max(axis=1, keepdims=True))
+    return E / E.sum(axis=1, keepdims=True)
+
+
+def eq3_objective_kld(A, B, bias, codes, T, T0, lam) -> float:
+    """Eq. 3 with the KL-divergence first term the paper prefers:
+    sum over rows of KL(softmax(a B + bias) || softmax(g T + bias)) + lam ||T - P0 B||^2, fp64.
+    KL(p || q) = sum_m p_m (log p_m - log q_m), logs from log-softmax (x - max - log sum exp)."""
+    G = onehot(codes)
+    C = codes.shape[1]
+    M = B.shape[1]
+    Y = np.asarray(A, np.float64) @ np.asarray(B, np.float64) + np.asarray(bias, np.float64)
+    Z = G @ np.asarray(T, np.float64).reshape(K * C, M) + np.asarray(bias, np.float64)
+
+    def log_softmax(X):
+        Xs = X - X.max(axis=1, keepdims=True)
+        return Xs - np.log(np.exp(Xs).sum(axis=1, keepdims=True))
+    lp, lq = log_softmax(Y), log_softmax(Z)
+    kl = float((np.exp(lp) * (lp - lq)).sum())
+    return kl + lam * float(((np.asarray(T, np.float64) - np.asarray(T0, np.float64)) ** 2).sum())
+
+
+def eq3_kld_grad(A, B, bias, codes, T, T0, lam) -> np.ndarray:
+    """Analytic gradient of eq3_objective_kld in T: with p = softmax(Y), q = softmax(Z), Z = G T + bias,
+    d/dZ KL(p || q) = q - p per row, so dJ/dT = G^T (q - p) + 2 lam (T - T0); [C][16][M]."""
+    G = onehot(codes)
+    C = codes.shape[1]
+    M = B.shape[1]
+    Y = np.asarray(A, np.float64) @ np.asarray(B, np.float64) + np.asarray(bias, np.float64)
+    Z = G @ np.asarray(T, np.float64).reshape(K * C, M) + np.asarray(bias, np.float64)
+    g = G.T @ (softmax_rows(Z) - softmax_rows(Y))
+    return g.reshape(C, K, M) + 2.0 * lam * (np.asarray(T, np.float64) - np.asarray(T0, np.float64))
+
+
+def optimize_lut_kld(A, B, bias, codes, T0, lam, steps: int, lr: float) -> np.ndarray:
+    """Eq. 3 with the KLD objective minimised by plain gradient descent from T = P0 B (the paper gives
+    no optimiser; reading R23 in DESIGN.md): `steps` updates T <- T - lr * eq3_kld_grad(T), fp64."""
+    T = np.asarray(T0, np.float64).copy()
+    for _ in range(int(steps)):
+        T = T - lr * eq3_kld_grad(A, B, bias, codes, T, T0, lam)
+    return T
+
+
 def requantize(params: dict, T: np.ndarray) -> dict:
     """Same trees, LUT from table T through the same uint8 quantiser (reading R6)."""
     q, scale, lo = quantize(np.asarray(T, np.float64))

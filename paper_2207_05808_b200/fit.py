@@ -79,11 +79,82 @@ def _fit_subspace(X: np.ndarray):
     return split, thr, P
 
 
+def fit_trees_gpu(Xall: np.ndarray, bnd: np.ndarray, device: int = 0):
+    """Depth-4 trees of all C subspaces at once on the GPU (readings R3/R4; SURVEY f4 "tree fitting at
+    BASELINE scale"), fp64 torch ops batched over codebooks: per level the pooled within-node sum of
+    squares of every dim (segment sums by scatter_add), its argmax (first maximum = smallest dim on
+    ties), and each node's lower median on the chosen dim (a stable sort of the node's values).
+    Returns split [C][4], thresholds [C][15] (fp64 data values) and the leaf of every row [n][C].
+    The leaf assignment decides the prototypes, which the caller averages on the host exactly as the
+    oracle does, so the LUT is bit-identical whenever the split dims agree (their SSE sums differ from
+    numpy's only in rounding order)."""
+    import torch
+    dev = torch.device("cuda", device)
+    n = Xall.shape[0]
+    C = len(bnd) - 1
+    dmax = int(np.max(np.diff(bnd)))
+    # [C][n][dmax] fp64, padded dims hold 0 (their SSE is 0: never chosen unless every dim is constant,
+    # where the first dim wins in both implementations)
+    Xc = np.zeros((C, n, dmax))
+    for c in range(C):
+        Xc[c, :, : bnd[c + 1] - bnd[c]] = Xall[:, bnd[c]:bnd[c + 1]]
+    X = torch.from_numpy(Xc).to(dev)
+    leaf = torch.zeros((C, n), dtype=torch.int64, device=dev)
+    split = torch.zeros((C, N_LEVELS), dtype=torch.int64, device=dev)
+    thr = torch.zeros((C, 2 ** N_LEVELS - 1), dtype=torch.float64, device=dev)
+    crange = torch.arange(C, device=dev)
+    for t in range(N_LEVELS):
+        nn = 2 ** t
+        seg = (crange[:, None] * nn + leaf).reshape(-1)                     # (c, node) segment of each row
+        cnt = torch.bincount(seg, minlength=C * nn).to(torch.float64)
+        sums = torch.zeros((C * nn, dmax), dtype=torch.float64, device=dev).index_add_(0, seg, X.reshape(-1, dmax))
+        means = sums / cnt.clamp(min=1)[:, None]
+        dev2 = (X.reshape(-1, dmax) - means[seg]) ** 2
+        sse = torch.zeros((C * nn, dmax), dtype=torch.float64, device=dev).index_add_(0, seg, dev2)
+        j = torch.argmax(sse.reshape(C, nn, dmax).sum(dim=1), dim=1)    # [C]; first maximum on ties
+        split[:, t] = j
+        v = X[crange, :, j]                                                 # [C][n] values on the split dim
+        # lower median per node: stable sort by value, then stable by node -> node segments in value order
+        o1 = torch.argsort(v, dim=1, stable=True)
+        o2 = torch.argsort(torch.gather(leaf, 1, o1), dim=1, stable=True)
+        order = torch.gather(o1, 1, o2)
+        sv = torch.gather(v, 1, order)
+        cnt_n = cnt.reshape(C, nn).long()
+        starts = torch.cumsum(cnt_n, dim=1) - cnt_n
+        mid = (starts + (cnt_n - 1).clamp(min=0) // 2).clamp(max=n - 1)
+        med = torch.gather(sv, 1, mid)
+        base = 2 ** t - 1
+        for node in range(nn):                                              # empty node: parent's threshold
+            h = base + node
+            parent = thr[:, (h - 1) // 2] if h > 0 else torch.zeros(C, dtype=torch.float64, device=dev)
+            thr[:, h] = torch.where(cnt_n[:, node] > 0, med[:, node], parent)
+        leaf = 2 * leaf + (v > torch.gather(thr, 1, base + leaf)).long()
+    return split.cpu().numpy().astype(np.int32), thr.cpu().numpy(), leaf.t().contiguous().cpu().numpy()
+
+
+def _prototypes_from_leaves(X: np.ndarray, leaf: np.ndarray) -> np.ndarray:
+    """Leaf-mean prototypes (R5) from a leaf assignment, with the oracle's reductions: node mean =
+    numpy mean over the node's rows in ascending row order; an empty leaf takes its nearest
+    non-empty ancestor's mean."""
+    P = np.zeros((N_PROTO, X.shape[1]))
+    for k in range(N_PROTO):
+        for t in range(N_LEVELS, -1, -1):
+            node = k >> (N_LEVELS - t)
+            rows = np.nonzero((leaf >> (N_LEVELS - t)) == node)[0]
+            if len(rows):
+                P[k] = X[rows].mean(axis=0)
+                break
+    return P
+
+
 def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | None = None,
-              bias: np.ndarray | None = None, a_is_bf16: bool = False) -> dict:
-    """Fit trees and the quantised LUT of one layer approximating A @ B (+ bias).
+              bias: np.ndarray | None = None, a_is_bf16: bool = False, device: int | None = None) -> dict:
+    """Fit trees and the quantised LUT of one layer approximating A @ B (+ bias).  device=None fits
+    the trees on the host; device=k fits them on GPU k (fit_trees_gpu) — same parameters.
 
     Returns the parameter dict consumed by :class:`paper_2207_05808_b200.Plan`."""
+    if device is not None:
+        return _fit_layer_gpu_trees(A_train, B, C, perm, bias, a_is_bf16, device)
     A = np.asarray(A_train)
     if a_is_bf16:
         A = (A.astype(np.uint32) << 16).view(np.float32)
@@ -106,6 +177,31 @@ def fit_layer(A_train: np.ndarray, B: np.ndarray, C: int, perm: np.ndarray | Non
             T[c] += P[:, j:j + 1] * Bc[j:j + 1, :]
     q, scale, lo = quantize_table(T)
     return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr,
+                lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
+                bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)), T=T)
+
+
+def _fit_layer_gpu_trees(A_train, B, C, perm, bias, a_is_bf16, device):
+    A = np.asarray(A_train)
+    if a_is_bf16:
+        A = (A.astype(np.uint32) << 16).view(np.float32)
+    A = A.astype(np.float32)
+    D = A.shape[1]
+    B = np.asarray(B, dtype=np.float64)
+    M = B.shape[1]
+    perm = np.arange(D, dtype=np.int32) if perm is None else np.asarray(perm, dtype=np.int32)
+    bnd = chunk_bounds(D, C)
+    Xall = A[:, perm].astype(np.float64)
+    Bp = B[perm]
+    split, thr64, leaf = fit_trees_gpu(Xall, bnd, device)
+    T = np.zeros((C, N_PROTO, M))
+    for c in range(C):
+        P = _prototypes_from_leaves(Xall[:, bnd[c]:bnd[c + 1]], leaf[:, c])
+        Bc = Bp[bnd[c]:bnd[c + 1]]
+        for j in range(P.shape[1]):
+            T[c] += P[:, j:j + 1] * Bc[j:j + 1, :]
+    q, scale, lo = quantize_table(T)
+    return dict(D=D, C=C, M=M, perm=perm, boundaries=bnd, split_dim=split, thresholds=thr64.astype(np.float32),
                 lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32),
                 bias=(np.zeros(M, np.float32) if bias is None else np.asarray(bias, np.float32)), T=T)
 
@@ -172,14 +268,20 @@ def fit_mlp(A_train: np.ndarray, Bs: list, Cs: list, perms: list, biases: list, 
 
 
 def optimize_lut(params: dict, A_train: np.ndarray, B: np.ndarray, lam: float = 1.0, relu: bool = False,
-                 iters: int = 200, lr: float = 1e-2, device: int = 0, a_is_bf16: bool = False) -> dict:
+                 iters: int = 200, lr: float = 1e-2, device: int = 0, a_is_bf16: bool = False,
+                 objective: str = "mse") -> dict:
     """ITLUMM model-aware LUT optimisation, Eq. 3, on the GPU:
     argmin_T ||sigma(A B) - sigma(G T)||^2 + lam ||T - P0 B||^2, sigma = + bias (then ReLU when
     `relu`).  G comes from the plan's own encode kernel on the training rows.  Without a
     nonlinearity the bias cancels and T solves the normal equations (G^T G + lam I) T = G^T A B +
     lam P0 B (fp64, cuSOLVER through torch.linalg); with ReLU that solution seeds `iters` Adam steps
-    on the ReLU objective.  Returns the parameters with the new table requantised (same trees), so
-    the hot path is unchanged."""
+    on the ReLU objective.
+    objective="kld": sigma = bias then a row-wise softmax, first term sum over rows of
+    KL(softmax(a B + b) || softmax(g T + b)) (the objective the paper finds better; SPEC
+    S:343), minimised by `iters` steps of plain gradient descent from T = P0 B with the analytic
+    gradient G^T (softmax(G T + b) - softmax(A B + b)) + 2 lam (T - P0 B) (reading R23), fp64.
+    Returns the parameters with the new table requantised (same trees), so the hot path is unchanged
+    (P:131)."""
     import torch
     from .api import Plan
 
@@ -202,6 +304,19 @@ def optimize_lut(params: dict, A_train: np.ndarray, B: np.ndarray, lam: float = 
     G.scatter_(1, codes + 16 * torch.arange(C, device=dev), 1.0)
     Y = Af @ torch.from_numpy(np.asarray(B, np.float64)).to(dev)
     T0 = torch.from_numpy(np.asarray(params["T"], np.float64).reshape(16 * C, M)).to(dev)
+    if objective == "kld":
+        b = torch.from_numpy(np.asarray(params["bias"], np.float64)).to(dev)
+        Pt = torch.softmax(Y + b, dim=1)
+        T = T0.clone()
+        for _ in range(int(iters)):
+            T = T - lr * (G.T @ (torch.softmax(G @ T + b, dim=1) - Pt) + 2.0 * lam * (T - T0))
+        Tn = T.reshape(C, 16, M).cpu().numpy()
+        q, scale, lo = quantize_table(Tn)
+        out = dict(params)
+        out.update(lut=q, scale=scale.astype(np.float32), offset=lo.astype(np.float32), T=Tn)
+        return out
+    if objective != "mse":
+        raise ValueError(f"objective must be 'mse' or 'kld', got {objective!r}")
     lhs = G.T @ G + lam * torch.eye(16 * C, dtype=torch.float64, device=dev)
     T = torch.linalg.solve(lhs, G.T @ Y + lam * T0)
     if relu:

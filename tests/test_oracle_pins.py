@@ -539,3 +539,91 @@ def test_eq3_linear_optimality_and_limits():
         assert f(T) <= f(Tp)
     Tbig = ofit.optimize_lut_linear(A, B, codes, T0, 1e9)
     assert np.abs(Tbig - T0).max() < 1e-5
+
+
+# ---------------------------------------------------------------------------- f4: Eq. 3 with KLD
+def test_eq3_kld_hand_computed_value():
+    """KLD objective (P:100 softmax sigma) on a case worked by hand.
+    D = 1, M = 2, C = 1, bias 0: row 1 a = 1, B = [[0, ln 3]] -> softmax(aB) = (1/4, 3/4); code 0 with
+    T[0][0] = (0, 0) -> q = (1/2, 1/2); KL = 1/4 ln(1/2) + 3/4 ln(3/2).  Row 2 a = 0 -> p = (1/2, 1/2);
+    code 1 with T[0][1] = (ln 3, 0) -> q = (3/4, 1/4); KL = 1/2 ln(2/3) + 1/2 ln 2.  With T0 = 0 and
+    lam = 0.5 the penalty is 0.5 (ln 3)^2."""
+    A = np.array([[1.0], [0.0]])
+    B = np.array([[0.0, math.log(3.0)]])
+    codes = np.array([[0], [1]], np.uint8)
+    T = np.zeros((1, 16, 2))
+    T[0, 1, 0] = math.log(3.0)
+    want_kl = 0.25 * math.log(0.5) + 0.75 * math.log(1.5) + 0.5 * math.log(2.0 / 3.0) + 0.5 * math.log(2.0)
+    assert ofit.eq3_objective_kld(A, B, np.zeros(2), codes, T, T, 0.5) == pytest.approx(want_kl, abs=1e-14)
+    want = want_kl + 0.5 * math.log(3.0) ** 2
+    assert ofit.eq3_objective_kld(A, B, np.zeros(2), codes, T, np.zeros_like(T), 0.5) == pytest.approx(want, abs=1e-14)
+
+
+def test_eq3_kld_gradient_matches_central_differences():
+    """SPEC S:344 example: softmax + KLD on a random 64 x 16 x 10 instance (64 rows, one codebook of
+    16 codes, M = 10): the analytic gradient matches central finite differences to rel. err < 1e-4."""
+    rng = np.random.default_rng(5)
+    N, D, M = 64, 6, 10
+    A, B, bias = rng.normal(size=(N, D)), rng.normal(size=(D, M)), rng.normal(size=M)
+    codes = rng.integers(0, 16, size=(N, 1)).astype(np.uint8)
+    T0 = rng.normal(size=(1, 16, M))
+    T = T0 + 0.3 * rng.normal(size=T0.shape)
+    g = ofit.eq3_kld_grad(A, B, bias, codes, T, T0, 0.7)
+    h = 1e-6
+    num = np.zeros_like(T)
+    for idx in np.ndindex(T.shape):
+        Tp, Tm = T.copy(), T.copy()
+        Tp[idx] += h
+        Tm[idx] -= h
+        num[idx] = (ofit.eq3_objective_kld(A, B, bias, codes, Tp, T0, 0.7) -
+                    ofit.eq3_objective_kld(A, B, bias, codes, Tm, T0, 0.7)) / (2 * h)
+    assert np.abs(g - num).max() / np.abs(num).max() < 1e-4
+
+
+def test_eq3_kld_softmax_shift_invariance():
+    """softmax is invariant to adding one constant to a whole row, and every row holds exactly one
+    code per codebook: adding kappa to all 16 entries of codebook c, in every column, adds kappa to
+    every row of G T, which leaves the KL term unchanged; and the KL gradient sums to 0 over the
+    outputs m of each (c, k)."""
+    rng = np.random.default_rng(6)
+    N, D, M, C = 50, 8, 7, 3
+    A, B, bias = rng.normal(size=(N, D)), rng.normal(size=(D, M)), rng.normal(size=M)
+    codes = rng.integers(0, 16, size=(N, C)).astype(np.uint8)
+    T = rng.normal(size=(C, 16, M))
+    T2 = T.copy()
+    T2[1] += 2.5
+    f = lambda TT: ofit.eq3_objective_kld(A, B, bias, codes, TT, TT, 0.0)  # noqa: E731
+    assert f(T2) == pytest.approx(f(T), rel=1e-12, abs=1e-12)
+    g = ofit.eq3_kld_grad(A, B, bias, codes, T, T, 0.0)
+    assert np.abs(g.sum(axis=2)).max() < 1e-12
+
+
+def test_eq3_kld_exact_reconstruction_is_a_fixed_point():
+    """SPEC S:344 example: when G reconstructs A B exactly (exact PQ, rows equal prototypes), T = P0 B
+    already gives a zero KL term and a zero gradient, so the descent returns T0 unchanged."""
+    C, M = 4, 6
+    A_train, _, kt, B, bias = exact_pq_case(C, M, n_rep=2, seed=7)
+    p = ofit.fit(A_train, B, C, np.arange(4 * C), bias)
+    codes = oracle.amm(p, A_train, relu=False, want_codes=True)["codes"]
+    T0 = p["T"]
+    assert ofit.eq3_objective_kld(A_train, B, bias, codes, T0, T0, 0.3) < 1e-12
+    assert np.abs(ofit.eq3_kld_grad(A_train, B, bias, codes, T0, T0, 0.3)).max() < 1e-12
+    T = ofit.optimize_lut_kld(A_train, B, bias, codes, T0, 0.3, steps=5, lr=0.1)
+    assert np.abs(T - T0).max() < 1e-12
+
+
+def test_eq3_kld_descent_lowers_the_objective():
+    """Gradient descent with a small step lowers the KLD objective at every step (fixed-step GD on a
+    smooth convex-in-Z objective) and ends below T0."""
+    rng = np.random.default_rng(9)
+    N, D, M, C = 200, 12, 5, 3
+    A, B, bias = rng.normal(size=(N, D)), rng.normal(size=(D, M)), rng.normal(size=M)
+    codes = rng.integers(0, 16, size=(N, C)).astype(np.uint8)
+    T0 = rng.normal(size=(C, 16, M))
+    f = lambda TT: ofit.eq3_objective_kld(A, B, bias, codes, TT, T0, 0.05)  # noqa: E731
+    vals = [f(T0)]
+    T = T0
+    for _ in range(10):
+        T = T - 0.02 * ofit.eq3_kld_grad(A, B, bias, codes, T, T0, 0.05)
+        vals.append(f(T))
+    assert all(b < a for a, b in zip(vals, vals[1:]))

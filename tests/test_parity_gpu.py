@@ -422,6 +422,42 @@ def test_eq3_lut_optimisation_gpu_vs_oracle():
     assert_out(y.cpu().numpy(), oracle.amm(rel_o, w["A"], relu=True, nthreads=8)["y"])
 
 
+def test_eq3_kld_lut_optimisation_gpu_vs_oracle():
+    """f4 with the KLD objective (P:100 softmax sigma): the GPU descent (codes
+    from the encode kernel, fp64 torch) follows the oracle's fp64 descent step for step (same start
+    P0 B, same steps, same rate; only the summation order differs), lowers the oracle's KLD objective,
+    quantises to the same LUT, and that layer keeps kernel/oracle parity."""
+    from paper_2207_05808_b200 import Plan
+    from paper_2207_05808_b200.fit import optimize_lut
+    w = synth.small_case(42, N=1500, D=80, M=12, C=6, n_train=1200)
+    po = ofit.fit(w["A_train"], w["B"], 6, w["perm"], w["bias"])
+    gpu = optimize_lut(po, w["A_train"], w["B"], lam=0.2, iters=40, lr=2e-3, objective="kld")
+    codes = oracle.amm(po, w["A_train"], relu=False, want_codes=True, nthreads=8)["codes"]
+    Tref = ofit.optimize_lut_kld(w["A_train"], w["B"], w["bias"], codes, po["T"], 0.2, steps=40, lr=2e-3)
+    assert np.abs(gpu["T"] - Tref).max() <= 1e-9 * (1 + np.abs(Tref).max())
+    f = lambda T: ofit.eq3_objective_kld(w["A_train"], w["B"], w["bias"], codes, T, po["T"], 0.2)  # noqa: E731
+    assert f(Tref) < f(po["T"])
+    ro = ofit.requantize(po, Tref)
+    assert np.array_equal(gpu["lut"], ro["lut"]) and np.array_equal(gpu["scale"], ro["scale"])
+    y = Plan(ro).amm(torch.from_numpy(w["A"]).cuda(), relu=False)
+    torch.cuda.synchronize()
+    assert_out(y.cpu().numpy(), oracle.amm(ro, w["A"], relu=False, nthreads=8)["y"])
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3_c64", "cfg5"])
+def test_gpu_tree_fit_equals_oracle_at_baseline_scale(name):
+    """f4 tree fitting on the GPU (fit_trees_gpu: batched per-level SSE and lower medians) at the
+    BASELINE configs' training sizes: split dims, thresholds and the whole fitted layer (LUT, scale,
+    offset) bit-identical to the oracle's plain per-node fit (R3-R5)."""
+    from paper_2207_05808_b200 import fit_layer
+    w = synth.workload(name, n_rows=0)
+    bf16 = w["dtype"] == "bf16"
+    pg = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16, device=0)
+    po = ofit.fit(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
+    for k in ("split_dim", "thresholds", "lut", "scale", "offset"):
+        assert np.array_equal(np.asarray(pg[k]).view(np.uint8), np.asarray(po[k]).view(np.uint8)), k
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_strided_rows_bulk_copy_path_and_scratch_chunking(dtype):
     """Rows with lda > D but 16-byte aligned go through the per-row bulk copies of the streaming
