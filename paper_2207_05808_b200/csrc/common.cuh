@@ -75,34 +75,23 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
-// Blocking wait for the phase with `parity` to complete.  try_wait with a suspend-time hint parks
-// the thread in hardware until the phase completes (or 1 ms passes), so waiting warps do not spin
-// and take issue slots from the warps they wait for (a spinning wait made the k_tcp producers sharing
-// an SM sub-partition with them ~2x slower, tcp_trace in profiles/r02).  After ~5 s of waiting the
-// kernel traps, so a broken pipeline protocol surfaces as a launch error instead of a hung GPU.
+// Blocking wait for the phase with `parity` to complete: try_wait (the hardware suspends the
+// thread for a short, system-defined window per attempt).  After ~2^28 attempts the kernel traps,
+// so a broken pipeline protocol surfaces as a launch error instead of a hung GPU.  (A 1 ms
+// suspend-time hint compiles to NANOSLEEP.SYNCS, which wakes at any barrier event of the SM: no
+// fewer re-checks, and measured no faster; tools/probes/ring_probe.cu gives the ring's costs.)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   for (uint32_t it = 0;; ++it) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
-    if (ok) return;
-    if (it > 5000u) __trap();
-  }
-}
-// Spin on mbarrier.test_wait (never suspends): lowest wake-up latency, costs issue slots.
-__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  for (uint32_t it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     if (ok) return;
-    if (it > (1u << 30)) __trap();
+    if (it > (1u << 28)) __trap();
   }
 }
+
 // Non-blocking test of a phase (warp-uniform when all lanes test the same barrier).
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -127,18 +116,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
     if (ok) return;
     __nanosleep(ns);
     if (it > (1u << 26)) __trap();
-  }
-}
-// try_wait without a suspend-time hint (the hardware's default suspension window).
-__device__ __forceinline__ void mbar_wait_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  for (uint32_t it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    if (ok) return;
-    if (it > (1u << 28)) __trap();
   }
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -85,6 +85,9 @@ struct TcKArgs {
   int stream_b;
   int ST;          // ring stages
   int out_hint;    // L2 policy of the output tensor stores (l2_policy kind; 0 = default)
+  int dbg;         // developer removal switches (ITLUMM_TC_DBG; results then wrong): 1 producers skip
+                   // the one-hot stores, 2 no MMAs (commits only), 4 no LUT copies, 16 epilogue
+                   // skips the output stores, 32 no epilogue work
   uint64_t* trace; // developer timeline (ITLUMM_TC_TRACE): [8 CTAs][4 roles][kTraceEv] globaltimer stamps
 };
 constexpr int kTraceEv = 512;
@@ -410,8 +413,12 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           const uint8_t* src = g.qt + (size_t)sl * KB * bbytes;
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(empty_bar + stage, phase ^ 1);
-            mbar_arrive_expect_tx(full_bar + stage, bbytes);
-            bulk_g2s(b_s + (size_t)stage * bbytes, src + (size_t)kb * bbytes, bbytes, full_bar + stage);
+            if (g.dbg & 4) {
+              mbar_arrive(full_bar + stage);
+            } else {
+              mbar_arrive_expect_tx(full_bar + stage, bbytes);
+              bulk_g2s(b_s + (size_t)stage * bbytes, src + (size_t)kb * bbytes, bbytes, full_bar + stage);
+            }
             stamp(3);
             if (++stage == ST) { stage = 0; phase ^= 1; }
           }
@@ -445,8 +452,8 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
           uint32_t code[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) code[j] = (valid && kb * 8 + j < C) ? (cw >> (4 * j)) & 15u : 16u;
-          mbar_wait_sleep(empty_bar + stage, phase ^ 1, 32);   // MMA finished reading this stage
-          put_onehot<SP>(a_s + (size_t)stage * kAStage, r, code);
+          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
+          if (!(g.dbg & 1)) put_onehot<SP>(a_s + (size_t)stage * kAStage, r, code);
           fence_proxy_async_smem();
           mbar_arrive(full_bar + stage);
           if (r == 0) stamp(0);
@@ -559,17 +566,17 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait_sleep(acce_bar + acc, acc_phase ^ 1, 32);   // epilogue drained this accumulator
+        mbar_wait(acce_bar + acc, acc_phase ^ 1);    // epilogue drained this accumulator
         if (lane == 0) stamp(1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(full_bar + stage, phase);
-          tc_fence_after();
           const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((SB ? stage : kb) * b_step);
           if (elect_one()) {
-            if (SP) {
+            if (g.dbg & 2) {
+            } else if (SP) {
               // metadata rows -> TMEM columns 2NS + 4*stage (in tcgen05 issue order before the MMAs
               // that read them), then 2 sparse MMAs of K = 64 (4 codebooks each; A +32 B, B +64 B)
               const uint32_t e = tmem_base + (uint32_t)(2 * NS + 4 * stage);
@@ -615,7 +622,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       int sl, c0, c1;
       const uint64_t opol = l2_policy(g.out_hint);
       for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
-        mbar_wait_sleep(accf_bar + acc, acc_phase, 128);
+        mbar_wait(accf_bar + acc, acc_phase);
         tc_fence_after();
         if (warp == kTcEpiWarp0 && lane == 0) stamp(2);
         const int m0 = sl * NS;
@@ -623,7 +630,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         const float* otp = SB ? p.offtot + m0 : ot_s;
         const int row0 = (int)(tile * kTcRows) + q * 32;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
-        for (int j0 = (c0 + ((h - c0) & 1)) * 32; j0 < c1 * 32; j0 += 64) {
+        for (int j0 = (c0 + ((h - c0) & 1)) * 32; j0 < c1 * 32 && !(g.dbg & 32); j0 += 64) {
           uint32_t v[32];
           tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
           tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -654,12 +661,12 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
                 make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(g.dbg & 16)) {
             if (g.out_hint) tma_store_2d_hint(out_map, stg, m0 + j0, row0, opol);
             else tma_store_2d(out_map, stg, m0 + j0, row0);
             bulk_commit();
           }
-          pending = true;
+          pending = !(g.dbg & 16);
         }
         tc_fence_before();
         mbar_arrive(acce_bar + acc);
@@ -678,7 +685,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     int64_t tile;
     int sl, c0, c1;
     for (int64_t k = 0; item4(k, tile, sl, c0, c1); ++k) {
-      mbar_wait_sleep(accf_bar + acc, acc_phase, 128);
+      mbar_wait(accf_bar + acc, acc_phase);
       tc_fence_after();
       const int m0 = sl * NS;
       if (sl != cur_sl) {                             // this lane's scale/offtot, per slice
@@ -924,6 +931,8 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   k.trace = t.trace;
   static const int out_hint = getenv("ITLUMM_OUT_HINT") ? atoi(getenv("ITLUMM_OUT_HINT")) : 0;   // developer
   k.out_hint = out_hint;
+  static const int dbg = getenv("ITLUMM_TC_DBG") ? atoi(getenv("ITLUMM_TC_DBG")) : 0;   // developer
+  k.dbg = dbg;
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
   k.tma_store = (!a.acc && make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) ? 1 : 0;
@@ -935,8 +944,10 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   }
   k.CS = 0;
   if (!fused && a.ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(a.codes) & 15) == 0) {
-    // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest
-    for (int cs = 4; cs >= 1; --cs) {
+    // codes by bulk copy: as many 128-row stages (up to 4) as fit next to the rest (developer
+    // override, not ABI: ITLUMM_TC_CS = max codes stages; 0 = producers load codes with __ldg)
+    static const int cs_env = getenv("ITLUMM_TC_CS") ? atoi(getenv("ITLUMM_TC_CS")) : 4;
+    for (int cs = cs_env; cs >= 1; --cs) {
       const size_t need = tc_smem_layout(t.C, t.KB, t.NS, cs, (int)a.ldc, t.stream_b, fused, t.ST, t.sp).total;
       if (need <= kSmemMax && (int64_t)kTcRows * a.ldc < (1 << 20)) { k.CS = cs; smem = need; break; }
     }

@@ -181,9 +181,7 @@ struct TcpKArgs {
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
                                        // 16 epilogue skips the output stores, 32 no epilogue work,
-                                       // 64 producers spin on test_wait, 256 producers try_wait,
-                                       // 1024 dense one-hot as zero chunk + one byte store,
-                                       // 2048 MMA warp waits with try_wait
+                                       // 1024 dense one-hot as zero chunk + one byte store
 };
 
 template <bool SP>
@@ -264,7 +262,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait_sleep(codes_empty + cs, cph ^ 1, 128);
+        mbar_wait(codes_empty + cs, cph ^ 1);
         const int64_t r0 = tile * 2 * kTcRows + (int64_t)rank * kTcRows;
         const int64_t rows = g.N - r0 < kTcRows ? (g.N - r0 > 0 ? g.N - r0 : 0) : kTcRows;
         if (rows > 0) {
@@ -276,7 +274,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         if (++cs == CS) { cs = 0; cph ^= 1; }
         const int y0 = (sl * KB) * NS + (int)rank * (NS / 2);
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait_sleep(empty_bar + st, ph ^ 1, 64);  // the pair's MMAs are done with the stage
+          mbar_wait(empty_bar + st, ph ^ 1);  // the pair's MMAs are done with the stage
           stamp(2 + (int)rank, k * KB + kb);
           if (g.dbg & 4) {
             if (rank == 0) mbar_arrive(full_bar + st);
@@ -320,9 +318,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           uint32_t code[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) code[j] = j < nv ? (cw >> (4 * j)) & 15u : 16u;
-          if (g.dbg & 64) mbar_wait_spin(empty_bar + st, ph ^ 1);
-          else if (g.dbg & 256) mbar_wait(empty_bar + st, ph ^ 1);
-          else mbar_wait_sleep(empty_bar + st, ph ^ 1, 32);
+          mbar_wait(empty_bar + st, ph ^ 1);
 
           uint8_t* stg_a = ring + (size_t)st * L.stage;
           if (g.dbg & 1) {
@@ -398,16 +394,13 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         }
       };
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait_sleep(acce_bar + acc, aph ^ 1, 64);   // both CTAs' epilogues drained this accumulator
+        mbar_wait(acce_bar + acc, aph ^ 1);   // both CTAs' epilogues drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
         for (int kb = 0; kb < KB;) {
           const int st1 = st + 1 == ST ? 0 : st + 1;
           const uint32_t ph1 = st + 1 == ST ? ph ^ 1 : ph;
-          // a short timed sleep, not try_wait: this warp shares its SMSP with two producer warps, and a
-          // try_wait suspension ends at any barrier event of the SM (a near-spin in this kernel)
-          if (g.dbg & 2048) mbar_wait(full_bar + st, ph);
-          else mbar_wait_sleep(full_bar + st, ph, 16);
+          mbar_wait(full_bar + st, ph);
           // the next stage too if it is already full (one issue pass for both), never wait for it
           const bool two = __shfl_sync(0xffffffffu, (int)(kb + 1 < KB && mbar_test(full_bar + st1, ph1)), 0) != 0;
           if (lane == 0) stamp(0, k * KB + kb);
@@ -439,7 +432,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     int64_t tile;
     int sl;
     for (int64_t k = 0; item(k, tile, sl); ++k) {
-      mbar_wait_sleep(accf_bar + acc, aph, 256);
+      mbar_wait(accf_bar + acc, aph);
       tc_fence_after();
 
       const int m0 = sl * NS;
