@@ -181,7 +181,8 @@ struct TcpKArgs {
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
                                        // 16 epilogue skips the output stores, 32 no epilogue work,
-                                       // 1024 dense one-hot as zero chunk + one byte store
+                                       // 1024 dense one-hot as zero chunk + one byte store,
+                                       // 4096 one ring stage per MMA issue pass
 };
 
 template <bool SP>
@@ -402,7 +403,8 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           const uint32_t ph1 = st + 1 == ST ? ph ^ 1 : ph;
           mbar_wait(full_bar + st, ph);
           // the next stage too if it is already full (one issue pass for both), never wait for it
-          const bool two = __shfl_sync(0xffffffffu, (int)(kb + 1 < KB && mbar_test(full_bar + st1, ph1)), 0) != 0;
+          const bool two = !(g.dbg & 4096) &&
+                           __shfl_sync(0xffffffffu, (int)(kb + 1 < KB && mbar_test(full_bar + st1, ph1)), 0) != 0;
           if (lane == 0) stamp(0, k * KB + kb);
           if (elect_one()) {
             issue(st, kb, d);
