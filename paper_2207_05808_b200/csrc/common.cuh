@@ -101,23 +101,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
-// For waits off the critical path (an epilogue waiting for a whole tile, a loader far ahead of its
-// consumers): test, then a plain timed sleep of `ns` before testing again.  A try_wait suspension
-// (NANOSLEEP.SYNCS) ends at ANY barrier event of the SM, and in a kernel whose barriers change every
-// few hundred cycles such a waiter spins: ncu counted 140M re-checks in one k_tcp launch, stealing
-// issue slots from the producer warps that share its SM sub-partition.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  uint32_t ok;
-  for (uint32_t it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    if (ok) return;
-    __nanosleep(ns);
-    if (it > (1u << 26)) __trap();
-  }
-}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -446,8 +446,8 @@ static itlumm_status check_dev(itlumm_plan P, const void* ptr, const char* what)
 }
 
 // Rows per stage R and ring depth S of the streaming encoder for rows of rb bytes, or false if
-// the rows cannot be bulk-copied.  pow2: R a power of two dividing 128 (TC_SP ready counters).
-static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2, int* Rout, int* Sout,
+// the rows cannot be bulk-copied.
+static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, int* Rout, int* Sout,
                        int inflight_override_kb = 0, int max_stages = 8) {
   // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
   // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
@@ -464,11 +464,6 @@ static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, bool pow2,
   int R = (int)std::max<int64_t>(want, ((int64_t)stage_kb * 1024) / rb);
   if ((int64_t)((R + want - 1) / want * want) * rb <= 64 * 1024) R = (R + want - 1) / want * want;
   if ((int64_t)R * rb > 64 * 1024) R = (int)std::max<int64_t>(1, (64 * 1024) / rb);
-  if (pow2) {
-    int r2 = 1;
-    while (r2 * 2 <= R && r2 * 2 <= 128) r2 *= 2;
-    R = r2;
-  }
   const int64_t infl = inflight_override_kb > 0 ? inflight_override_kb : inflight_kb;
   int S = (int)std::max<int64_t>(2, std::min<int64_t>(max_stages, (infl * 1024 + R * rb / 2) / (R * rb)));
   while (S >= 2 && enc_smem_bytes(P->C, R, S, (int)rb) > 200 * 1024) --S;
@@ -491,7 +486,7 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
   // the columns per thread when they touch few of them (cfg4 C=16 layer 1: 64 of 3072 columns).
   const bool sparse_cols = P->seg_frac[dtype == ITLUMM_BF16 ? 1 : 0] < 0.6;
   int R = 0, S = 0;
-  if (aligned && !sparse_cols && enc_tiling(P, rb, kEncConsumerWarps, false, &R, &S)) {
+  if (aligned && !sparse_cols && enc_tiling(P, rb, kEncConsumerWarps, &R, &S)) {
     {
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -40,7 +42,9 @@ __device__ __forceinline__ uint64_t mdesc(uint32_t saddr) {
 
 // mode: 0 per-thread arrive, 1 per-warp arrive, 2 per-CTA (named barrier + 1 arrive)
 template <int MODE, bool STORE, bool MMA, bool LOADB, int EPI>
-__global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const uint8_t* lut, float* gout) {
+__global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const uint8_t* lut, float* gout,
+                       const __grid_constant__ CUtensorMap omap_v) {
+  const CUtensorMap* omap = &omap_v;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
   uint8_t* ring = sm;                                    // ST x 48 KB (A 16 KB + B 32 KB)
@@ -257,6 +261,30 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
             }
             continue;
           }
+          if (EPI == 7) {
+            // as k_tc's epilogue: 32 rows x 32 fp32 box, 128B-swizzled staging, 2-D tensor store
+            uint8_t* stg = ring + 8192 + (warp & 7) * 4096 - 8192 * 0;
+            if (half == 0) {
+              // stage the first 16 columns now, the second 16 on the next half (one 32x32 box per j0)
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              *reinterpret_cast<uint4*>(stg + lane * 128 + (((c + 4 * half) ^ (lane & 7)) << 4)) =
+                  make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            if (half == 1) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                const int x = j0, y = (blockIdx.x * 128 + q * 32) % 16384;
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
+                             ::"l"(reinterpret_cast<uint64_t>(omap)), "r"(su32(stg)), "r"(x), "r"(y) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              }
+              __syncwarp();
+            }
+            continue;
+          }
           if (EPI == 4) {
             // staging in shared memory (the A region of stage 0 is reused: timing only) + 1-D bulk store
             uint8_t* stg = ring + 8192 + (warp & 7) * 1024;
@@ -293,6 +321,7 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
   if (warp == P) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
+static CUtensorMap g_omap;
 template <int MODE, bool STORE, bool MMA, bool LOADB, int EPI>
 static void run(int sms, int P, int ST, unsigned long long* d, const uint8_t* lut, float* gout) {
   const int stages = 32 * 640;
@@ -300,8 +329,8 @@ static void run(int sms, int P, int ST, unsigned long long* d, const uint8_t* lu
   auto k = k_ring<MODE, STORE, MMA, LOADB, EPI>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = 32 * (P + 2 + 8);
-  k<<<sms, threads, smem>>>(P, ST, 32 * 8, d, lut, gout);
-  k<<<sms, threads, smem>>>(P, ST, stages, d, lut, gout);
+  k<<<sms, threads, smem>>>(P, ST, 32 * 8, d, lut, gout, g_omap);
+  k<<<sms, threads, smem>>>(P, ST, stages, d, lut, gout, g_omap);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); exit(1); }
   unsigned long long cyc;
@@ -320,9 +349,21 @@ int main() {
   cudaMemset(lut, 1, 16 << 20);
   float* gout;
   cudaMalloc(&gout, 64 << 20);
-  run<7, true, true, true, 4>(sms, 4, 2, d, lut, gout);
-  run<7, true, true, true, 0>(sms, 4, 2, d, lut, gout);
-  run<6, true, true, true, 4>(sms, 4, 2, d, lut, gout);
-  run<3, true, true, true, 4>(sms, 4, 2, d, lut, gout);
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    const cuuint64_t dims[2] = {256, 16384};
+    const cuuint64_t strides[1] = {256 * 4};
+    const cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
+    CUresult r = enc(&g_omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, gout, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("tensor map failed\n"); return 1; }
+  }
+  run<3, true, true, true, 4>(sms, 4, 4, d, lut, gout);
+  run<3, true, true, true, 7>(sms, 4, 4, d, lut, gout);
+  run<3, true, true, true, 0>(sms, 4, 4, d, lut, gout);
+  run<3, true, true, true, 7>(sms, 4, 3, d, lut, gout);
   return 0;
 }
