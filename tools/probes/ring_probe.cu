@@ -43,7 +43,7 @@ __device__ __forceinline__ uint64_t mdesc(uint32_t saddr) {
 // mode: 0 per-thread arrive, 1 per-warp arrive, 2 per-CTA (named barrier + 1 arrive)
 template <int MODE, bool STORE, bool MMA, bool LOADB, int EPI>
 __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const uint8_t* lut, float* gout,
-                       const __grid_constant__ CUtensorMap omap_v) {
+                       const __grid_constant__ CUtensorMap omap_v, const uint8_t* ga) {
   const CUtensorMap* omap = &omap_v;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
@@ -59,7 +59,7 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
   const int nprod = 32 * P;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(full + s, (MODE == 0 || MODE >= 3 ? nprod : MODE == 1 ? P : 1) + (LOADB ? 1 : 0));
+      mbar_init(full + s, MODE == 8 ? 1 : (MODE == 0 || MODE >= 3 ? nprod : MODE == 1 ? P : 1) + (LOADB ? 1 : 0));
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) { mbar_init(accf + a, 1); mbar_init(acce + a, 8); }
@@ -74,7 +74,7 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tm = *slot;
   unsigned long long t0 = clock64();
-  if (warp < P) {
+  if (warp < P && MODE != 8) {
     int st = 0;
     uint32_t ph = 0;
     for (int i = 0; i < stages; ++i) {
@@ -216,10 +216,14 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
       uint32_t ph = 0;
       for (int i = 0; i < stages; ++i) {
         mbar_wait(empty + st, ph ^ 1);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + st)), "r"(32768) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + st)), "r"(MODE == 8 ? 49152 : 32768) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(su32(ring + (size_t)st * 49152 + 16384)), "l"(lut + (size_t)(i % 512) * 32768), "r"(32768),
                      "r"(su32(full + st)) : "memory");
+        if (MODE == 8)   // A from a 1 GB one-hot matrix in HBM: this CTA's rows, K-block i
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(ring + (size_t)st * 49152)), "l"(ga + ((size_t)blockIdx.x * 4096 + (size_t)(i % 4096)) * 16384 % (1ull << 30)),
+                       "r"(16384), "r"(su32(full + st)) : "memory");
         if (++st == ST) { st = 0; ph ^= 1; }
       }
     }
@@ -322,6 +326,7 @@ __global__ void k_ring(int P, int ST, int stages, unsigned long long* out, const
 }
 
 static CUtensorMap g_omap;
+static const uint8_t* g_a;
 template <int MODE, bool STORE, bool MMA, bool LOADB, int EPI>
 static void run(int sms, int P, int ST, unsigned long long* d, const uint8_t* lut, float* gout) {
   const int stages = 32 * 640;
@@ -329,14 +334,14 @@ static void run(int sms, int P, int ST, unsigned long long* d, const uint8_t* lu
   auto k = k_ring<MODE, STORE, MMA, LOADB, EPI>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = 32 * (P + 2 + 8);
-  k<<<sms, threads, smem>>>(P, ST, 32 * 8, d, lut, gout, g_omap);
-  k<<<sms, threads, smem>>>(P, ST, stages, d, lut, gout, g_omap);
+  k<<<sms, threads, smem>>>(P, ST, 32 * 8, d, lut, gout, g_omap, g_a);
+  k<<<sms, threads, smem>>>(P, ST, stages, d, lut, gout, g_omap, g_a);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); exit(1); }
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   printf("{\"mode\": \"%s\", \"store\": %d, \"mma\": %d, \"loadb\": %d, \"epi\": %d, \"producer_warps\": %d, \"stages_in_ring\": %d, \"cycles_per_stage\": %.1f}\n",
-         MODE == 0 ? "per-thread" : MODE == 1 ? "per-warp" : MODE == 2 ? "per-cta" : MODE == 3 ? "k_tc-producer" : MODE == 4 ? "5-sts" : MODE == 5 ? "2-threads-per-row" : MODE == 6 ? "A-in-TMEM N=192" : "A-in-TMEM N=224", (int)STORE, (int)MMA, (int)LOADB, (int)EPI, P, ST, (double)cyc / stages);
+         MODE == 0 ? "per-thread" : MODE == 1 ? "per-warp" : MODE == 2 ? "per-cta" : MODE == 3 ? "k_tc-producer" : MODE == 4 ? "5-sts" : MODE == 5 ? "2-threads-per-row" : MODE == 6 ? "A-in-TMEM N=192" : MODE == 7 ? "A-in-TMEM N=224" : "A by TMA from HBM", (int)STORE, (int)MMA, (int)LOADB, (int)EPI, P, ST, (double)cyc / stages);
 }
 
 int main() {
@@ -361,9 +366,14 @@ int main() {
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("tensor map failed\n"); return 1; }
   }
-  run<3, true, true, true, 4>(sms, 4, 4, d, lut, gout);
+  {
+    uint8_t* a;
+    cudaMalloc(&a, 1ull << 30);
+    cudaMemset(a, 1, 1ull << 30);
+    g_a = a;
+  }
   run<3, true, true, true, 7>(sms, 4, 4, d, lut, gout);
-  run<3, true, true, true, 0>(sms, 4, 4, d, lut, gout);
-  run<3, true, true, true, 7>(sms, 4, 3, d, lut, gout);
+  run<8, true, true, true, 7>(sms, 4, 4, d, lut, gout);
+  run<8, true, true, true, 0>(sms, 4, 4, d, lut, gout);
   return 0;
 }
