@@ -15,14 +15,15 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = ATOL = 1e-6
-# "_sp24" / "_dense": the same schedule with the one-hot operand forced to the 2:4-sparse form
-# (tcgen05.mma.sp) or the dense form; plain names use the library's choice (AUTO: sparse
-# on the CTA-pair streamed-LUT kernel, dense on the 1-CTA kernel)
-ALGOS = ["auto", "simt", "tc", "tc_pipe", "tc_sp24", "tc_pipe_sp24", "tc_pipe_dense"]
+# "_sp24" / "_dense" / "_sel": the same schedule with the one-hot operand forced to the 2:4-sparse
+# form (tcgen05.mma.sp), the dense form, or the selector form (the one-hot as sparsity
+# metadata over a constant A, CTA-pair kernel on every shape); plain names use the library's choice
+# (AUTO: selector on the CTA-pair streamed-LUT kernel, dense on the 1-CTA kernel)
+ALGOS = ["auto", "simt", "tc", "tc_pipe", "tc_sp24", "tc_pipe_sp24", "tc_pipe_dense", "tc_sel", "tc_pipe_sel"]
 
 
 def _set(plan, algo):
-    for suffix, onehot in (("_sp24", "sparse24"), ("_dense", "dense")):
+    for suffix, onehot in (("_sp24", "sparse24"), ("_dense", "dense"), ("_sel", "select")):
         if algo.endswith(suffix):
             plan.set_algo(algo[: -len(suffix)])
             plan.set_onehot(onehot)
@@ -76,7 +77,10 @@ def run_all(params, A, relu, dtype, algo):
     assert np.array_equal(unpack(codes.cpu().numpy(), params["C"]), ref["codes"])
     if params["C"] % 2:
         assert np.all(codes.cpu().numpy()[:, -1] >> 4 == 0)     # R14 padding nibble
-    _set(plan, algo)
+    try:
+        _set(plan, algo)
+    except ItlummError as e:
+        _skip_or_raise(algo, e)
     # the fused call and the two-step call are checked independently: a schedule that refuses one
     # of them must not hide the other
     skipped = []
@@ -334,7 +338,7 @@ def test_parity_one_cta_streamed_lut_kernel():
         "    ref = oracle.amm(p, w['A'], relu=w['relu'], dtype=dt, nthreads=8)['y']\n"
         "    A = torch.from_numpy(w['A'].view(np.int16) if dt == 'bf16' else w['A']).cuda()\n"
         "    A = A.view(torch.bfloat16) if dt == 'bf16' else A\n"
-        "    for oh in ('dense', 'sparse24'):\n"
+        "    for oh in ('dense', 'sparse24', 'select'):\n"
         "        pl = Plan(p); pl.set_onehot(oh)\n"
         "        y = pl.amm(A, relu=w['relu']).cpu().numpy()\n"
         "        assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), (seed, oh)\n"
@@ -372,8 +376,9 @@ def sample_rows(N: int, n: int, seed: int = 0) -> np.ndarray:
     return rows
 
 
-@pytest.mark.parametrize("name,onehot", [("cfg3_c64", "auto"), ("cfg3_c64", "sparse24"), ("cfg3_c128", "auto"),
-                                         ("cfg3_c128", "sparse24"), ("cfg5", "auto")])
+@pytest.mark.parametrize("name,onehot", [("cfg3_c64", "auto"), ("cfg3_c64", "sparse24"), ("cfg3_c64", "dense"),
+                                         ("cfg3_c128", "auto"), ("cfg3_c128", "sparse24"), ("cfg3_c128", "dense"),
+                                         ("cfg5", "auto"), ("cfg5", "dense")])
 def test_benched_streamed_lut_shapes_full_size_sampled(name, onehot):
     """BASELINE configs[2] (C = 64, 128) and configs[4] at FULL size in the launch configuration
     bench.py times (AUTO: encode -> CTA-pair tensor-core accumulate over a streamed LUT with several
