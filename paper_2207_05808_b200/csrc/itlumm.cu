@@ -575,7 +575,7 @@ static const TcPlan& tcp(itlumm_plan P) { return P->onehot == ITLUMM_ONEHOT_SPAR
 // Developer knob (not ABI): ITLUMM_PAIR=0 keeps streamed LUTs on k_tc.
 static itlumm_status launch_tc_acc(itlumm_plan P, const TcArgs& a, cudaStream_t s, bool pdl) {
   static const bool pair_on = !(getenv("ITLUMM_PAIR") && atoi(getenv("ITLUMM_PAIR")) == 0);
-  static const bool sel_auto = !(getenv("ITLUMM_SEL") && atoi(getenv("ITLUMM_SEL")) == 0);   // developer
+  static const bool sel_auto = getenv("ITLUMM_SEL") && atoi(getenv("ITLUMM_SEL")) != 0;   // developer
   const TcPlan& t = tcp(P);
   if (P->onehot == ITLUMM_ONEHOT_SELECT ||
       (pair_on && sel_auto && P->onehot == ITLUMM_ONEHOT_AUTO && t.ok && t.stream_b && P->pair_sel.ok)) {

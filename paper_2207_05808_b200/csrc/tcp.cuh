@@ -183,7 +183,7 @@ struct TcpSmem {
   size_t a_bytes, e_bytes, b_bytes, stage, ring, aconst, codes, stg, bar, tmem, trc, total;
 };
 constexpr int kTcpTrcSlots = 16, kTcpTrcWin = 64, kTcpTrcFirst = 96;   // developer timeline window
-__host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int CS, int ldc, bool trace = false) {
+__host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int CS, int ldc, bool trace = false, int SS = 1) {
   TcpSmem s{};
   const bool sp = mode == kTcpSparse, sel = mode == kTcpSel;
   s.a_bytes = sel ? 0 : sp ? (size_t)kSpA : (size_t)kTcRows * kKBlock;          // 8 KB compressed / 16 KB dense
@@ -191,7 +191,7 @@ __host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int
   s.b_bytes = sel ? (size_t)kSelBlocks * (NS / 2) * kSelBlk : (size_t)(NS / 2) * kKBlock;   // half a LUT K-block
   s.stage = (s.a_bytes + s.e_bytes + s.b_bytes + 1023) & ~(size_t)1023;
   s.ring = 0;
-  s.aconst = s.ring + (size_t)ST * s.stage;
+  s.aconst = s.ring + (size_t)ST * SS * s.stage;   // ST ring slots of SS sub-stages (one K-block each)
   s.codes = s.aconst + (sel ? (size_t)kSpA : 0);
   s.stg = s.codes + (((size_t)CS * kTcRows * ldc + 1023) & ~(size_t)1023);
   s.bar = s.stg + (size_t)kTcEpiWarps * kTcStage;
@@ -207,10 +207,14 @@ struct TcpKArgs {
   int32_t* acc; int64_t ldacc;         // optional raw int32 accumulators (then per-thread stores)
   float* out; int64_t ldo;
   int relu;
-  int KB, NS, G, ST, CS;                // KB: ring stages (8-codebook K-blocks) per item
+  int KB, NS, G, ST, CS;                // KB: 8-codebook K-blocks per item; ST ring slots
+  int SS;                              // K-blocks (sub-stages) per ring slot: one barrier round trip each
   int tmem_cols;
   int pdl;
   uint64_t* trace;                     // developer timeline (ITLUMM_TC_TRACE=1): [4 CTAs][4 roles][kTraceEv]
+  int cload;                           // codes tiles loaded by their own warp (16) instead of the LUT loader
+  int pbar;                            // producers arrive once per CTA (named barrier) instead of per warp
+  int group;                           // MMA issue: stages per pass (1-4), 0 = adaptive (test_wait probe)
   int dbg;                             // developer removal switches (ITLUMM_TCP_DBG; results then wrong):
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
@@ -225,8 +229,9 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   constexpr bool SP = MODE == kTcpSparse, SEL = MODE == kTcpSel;
   extern __shared__ __align__(1024) uint8_t smem_tcp[];
   uint8_t* smem = smem_tcp + ((1024u - (smem_u32(smem_tcp) & 1023u)) & 1023u);
-  const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, ST = g.ST, CS = g.CS;
-  const TcpSmem L = tcp_smem_layout(MODE, NS, ST, CS, (int)g.ldc, g.trace != nullptr);
+  const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, ST = g.ST, CS = g.CS, SS = g.SS;
+  const int KBS = KB / SS;                 // ring slots per item
+  const TcpSmem L = tcp_smem_layout(MODE, NS, ST, CS, (int)g.ldc, g.trace != nullptr, SS);
   // MMA width of slice sl: selector slices are NS wide except a narrower last one (whole 32-column
   // epilogue chunks), so that a 4096-column layer in 224-column slices runs no padding columns
   auto slice_n = [&](int sl) -> int {
@@ -271,7 +276,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, 2 * kTcpProdWarps + 1); mbar_init(empty_bar + s, 1); }
+    for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, (g.pbar ? 2 : 2 * kTcpProdWarps) + 1); mbar_init(empty_bar + s, 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, 2 * kTcpEpiWarps); }
     for (int s = 0; s < CS; ++s) { mbar_init(codes_full + s, 1); mbar_init(codes_empty + s, kTcpProdWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -301,7 +306,32 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   if (g.pdl) pdl_wait();
   pdl_launch_dependents();
 
-  if (warp == kTcpLoaderWarp) {
+  auto load_codes = [&](int64_t tile, int cs) {       // this CTA's 128-row codes tile of a pair tile
+    const int64_t r0 = tile * 2 * kTcRows + (int64_t)rank * kTcRows;
+    const int64_t rows = g.N - r0 < kTcRows ? (g.N - r0 > 0 ? g.N - r0 : 0) : kTcRows;
+    if (rows > 0) {
+      mbar_arrive_expect_tx(codes_full + cs, (uint32_t)(rows * g.ldc));
+      bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, (uint32_t)(rows * g.ldc), codes_full + cs);
+    } else {
+      mbar_arrive(codes_full + cs);                    // a pair tile's empty second half
+    }
+  };
+  if (g.cload && role == 18) {
+    // ================================================================ codes loader (own warp): up to
+    // CS items ahead of the producers, independent of the LUT ring (the LUT loader runs only ST
+    // slots ahead of the MMAs, too late to hide a codes tile's L2/HBM latency at an item boundary)
+    if (lane == 0) {
+      int cs = 0;
+      uint32_t cph = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k) {
+        mbar_wait(codes_empty + cs, cph ^ 1);
+        load_codes(tile, cs);
+        if (++cs == CS) { cs = 0; cph ^= 1; }
+      }
+    }
+  } else if (warp == kTcpLoaderWarp) {
     // ================================================================ loader (one lane per CTA)
     if (lane == 0) {
       const uint32_t bhalf = (uint32_t)(NS / 2) * kKBlock;
@@ -310,23 +340,18 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        mbar_wait(codes_empty + cs, cph ^ 1);
-        const int64_t r0 = tile * 2 * kTcRows + (int64_t)rank * kTcRows;
-        const int64_t rows = g.N - r0 < kTcRows ? (g.N - r0 > 0 ? g.N - r0 : 0) : kTcRows;
-        if (rows > 0) {
-          mbar_arrive_expect_tx(codes_full + cs, (uint32_t)(rows * g.ldc));
-          bulk_g2s(codes_s + (size_t)cs * kTcRows * g.ldc, g.codes + r0 * g.ldc, (uint32_t)(rows * g.ldc), codes_full + cs);
-        } else {
-          mbar_arrive(codes_full + cs);                  // a pair tile's empty second half
+        if (!g.cload) {
+          mbar_wait(codes_empty + cs, cph ^ 1);
+          load_codes(tile, cs);
+          if (++cs == CS) { cs = 0; cph ^= 1; }
         }
-        if (++cs == CS) { cs = 0; cph ^= 1; }
         const int y0 = (sl * KB) * NS + (int)rank * (NS / 2);
         // selector image: [G][3 KB][NS rows][64 B]; this CTA's rows of a block start at rank * n / 2
         const int ys = (sl * KB * kSelBlocks) * NS + (int)rank * (slice_n(sl) / 2);
         const uint32_t sbox = (uint32_t)(NS / 2) * kSelBlk;
-        for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(empty_bar + st, ph ^ 1);  // the pair's MMAs are done with the stage
-          stamp(2 + (int)rank, k * KB + kb);
+        for (int kb = 0; kb < KBS; ++kb) {
+          mbar_wait(empty_bar + st, ph ^ 1);  // the pair's MMAs are done with the slot
+          stamp(2 + (int)rank, k * KBS + kb);
           if (g.dbg & 4) {
             if (rank == 0) mbar_arrive(full_bar + st);
           } else if (SEL) {
@@ -336,9 +361,10 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
             for (int j = 0; j < kSelBlocks; ++j)
               tma_load_2d_pair(bs + j * sbox, &qt_map, 0, ys + (kb * kSelBlocks + j) * NS, full_leader + 8u * st);
           } else {
-            if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * bhalf);
-            tma_load_2d_pair(ring + (size_t)st * L.stage + L.a_bytes + L.e_bytes, &qt_map, 0, y0 + kb * NS,
-                             full_leader + 8u * st);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * bhalf * SS);
+            for (int j = 0; j < SS; ++j)
+              tma_load_2d_pair(ring + (size_t)(st * SS + j) * L.stage + L.a_bytes + L.e_bytes, &qt_map, 0,
+                               y0 + (kb * SS + j) * NS, full_leader + 8u * st);
           }
           if (++st == ST) { st = 0; ph ^= 1; }
         }
@@ -365,9 +391,11 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       uint4 quad = make_uint4(0, 0, 0, 0);
       // one ring stage per proxy fence and arrive: pairing stages made a stage wait for the NEXT
       // stage's slot to free up (one MMA pass later), which cost more than the fence it saved
-      for (int kb = 0; kb < KB; ++kb) {
-        {
-          const int kbi = kb;
+      for (int kb = 0; kb < KBS; ++kb) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          if (jj >= SS) break;
+          const int kbi = kb * SS + jj;
           if ((kbi & 3) == 0 && valid) quad = *reinterpret_cast<const uint4*>(crow + kbi * 4);   // 4 K-blocks of codes
           const uint32_t cw = ((kbi & 3) == 0 ? quad.x : (kbi & 3) == 1 ? quad.y : (kbi & 3) == 2 ? quad.z : quad.w) >> (16 * half);
           const int c0 = kbi * 8 + 4 * half;               // first codebook of this thread
@@ -375,9 +403,9 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           uint32_t code[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) code[j] = j < nv ? (cw >> (4 * j)) & 15u : 16u;
-          mbar_wait(empty_bar + st, ph ^ 1);
+          if (jj == 0) mbar_wait(empty_bar + st, ph ^ 1);
 
-          uint8_t* stg_a = ring + (size_t)st * L.stage;
+          uint8_t* stg_a = ring + (size_t)(st * SS + jj) * L.stage;
           if (g.dbg & 1) {
           } else if (SEL) {
             // 96 metadata bits of codebooks 4 half .. +3 at bits 96 half .. of the row's 192; bytes
@@ -416,9 +444,15 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           }
         }
         if (!(g.dbg & 8)) fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
-        if (lane == 0 && rank == 0) stamp(4 + role, k * KB + kb);
+        if (g.pbar) {
+          // one arrival per CTA: the 8 producer warps meet at a named barrier first
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcpProdWarps) : "memory");
+          if (role == 0 && lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
+        }
+        if (lane == 0 && rank == 0) stamp(4 + role, k * KBS + kb);
         if (++st == ST) { st = 0; ph ^= 1; }
       }
       __syncwarp();
@@ -475,28 +509,64 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           umma_i8_pair(d, ad + 6, bd + 6, idesc, 1u);
         }
       };
+      auto issue_slot = [&](int slot, int kb, uint32_t d) {   // the SS K-blocks of one ring slot
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (j < SS) issue(slot * SS + j, kb * SS + j, d);
+      };
       for (int64_t k = 0; item(k, tile, sl); ++k) {
         mbar_wait(acce_bar + acc, aph ^ 1);   // both CTAs' epilogues drained this accumulator
         tc_fence_after();
         if (SEL) idesc = idesc_i8_m256(slice_n(sl));
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
-        for (int kb = 0; kb < KB;) {
+        if (g.group > 0) {
+          // fixed groups of g.group stages per pass: wait for each (already-complete try_wait ~90
+          // cycles), then issue them all; no test_wait probe (~150 cycles) of the next stage
+          for (int kb = 0; kb < KBS;) {
+            const int np = KBS - kb < g.group ? KBS - kb : g.group;
+            int sts[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              sts[i] = st;
+              if (i < np) {
+                mbar_wait(full_bar + st, ph);
+                if (++st == ST) { st = 0; ph ^= 1; }
+              }
+            }
+            if (lane == 0) stamp(0, k * KBS + kb);
+            if (elect_one()) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (i < np) issue_slot(sts[i], kb + i, d);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (i < np) umma_commit_pair(empty_bar + sts[i]);
+              if (kb + np >= KBS) umma_commit_pair(accf_bar + acc);
+            }
+            __syncwarp();
+            if (lane == 0) stamp(1, k * KBS + kb);
+            kb += np;
+          }
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+          continue;
+        }
+        for (int kb = 0; kb < KBS;) {
           const int st1 = st + 1 == ST ? 0 : st + 1;
           const uint32_t ph1 = st + 1 == ST ? ph ^ 1 : ph;
           mbar_wait(full_bar + st, ph);
           // the next stage too if it is already full (one issue pass for both), never wait for it
           const bool two = !(g.dbg & 4096) &&
-                           __shfl_sync(0xffffffffu, (int)(kb + 1 < KB && mbar_test(full_bar + st1, ph1)), 0) != 0;
-          if (lane == 0) stamp(0, k * KB + kb);
+                           __shfl_sync(0xffffffffu, (int)(kb + 1 < KBS && mbar_test(full_bar + st1, ph1)), 0) != 0;
+          if (lane == 0) stamp(0, k * KBS + kb);
           if (elect_one()) {
-            issue(st, kb, d);
-            if (two) issue(st1, kb + 1, d);
+            issue_slot(st, kb, d);
+            if (two) issue_slot(st1, kb + 1, d);
             umma_commit_pair(empty_bar + st);
             if (two) umma_commit_pair(empty_bar + st1);
-            if (kb + (two ? 2 : 1) >= KB) umma_commit_pair(accf_bar + acc);
+            if (kb + (two ? 2 : 1) >= KBS) umma_commit_pair(accf_bar + acc);
           }
           __syncwarp();
-          if (lane == 0) stamp(1, k * KB + kb);
+          if (lane == 0) stamp(1, k * KBS + kb);
           st = two ? (st1 + 1 == ST ? 0 : st1 + 1) : st1;
           ph = two ? (st1 + 1 == ST ? ph1 ^ 1 : ph1) : ph1;
           kb += two ? 2 : 1;
@@ -597,7 +667,7 @@ struct TcpPlan {
   bool ok = false;
   const char* why = "not configured";
   int mode = kTcpDense;
-  int KB = 0, NS = 0, G = 0, ST = 0, tmem_cols = 512;
+  int KB = 0, NS = 0, G = 0, ST = 0, SS = 1, tmem_cols = 512;
   uint64_t* trace = nullptr;
   const uint8_t* qt = nullptr;         // dense/sparse: [G][KB][NS][128 B] swizzled K-major LUT slices;
                                        // selector: [G][3 KB][NS][64 B] (sel_layout_host)
@@ -639,8 +709,10 @@ inline void tcp_finish(TcpPlan& t, int C, int row_bytes) {
   t.ok = false;
   const int ldc_max = 16 * ((C + 31) / 32);
   static const int st_env = getenv("ITLUMM_TCP_STAGES") ? atoi(getenv("ITLUMM_TCP_STAGES")) : 0;   // developer
+  static const int ss_env = getenv("ITLUMM_TCP_SS") ? atoi(getenv("ITLUMM_TCP_SS")) : 2;   // developer
+  t.SS = (t.mode == kTcpDense && ss_env == 2 && t.KB % 2 == 0) ? 2 : 1;
   int ST = 12;
-  while (ST > 2 && tcp_smem_layout(t.mode, t.NS, ST, 2, ldc_max).total > kSmemMax) --ST;
+  while (ST > 2 && tcp_smem_layout(t.mode, t.NS, ST, 2, ldc_max, false, t.SS).total > kSmemMax) --ST;
   if (st_env >= 2 && st_env < ST) ST = st_env;
   const int meta_cols = t.mode == kTcpSel ? kSelMetaCols : t.mode == kTcpSparse ? 4 : 0;
   if (meta_cols && 2 * t.NS + meta_cols * ST > 512) ST = (512 - 2 * t.NS) / meta_cols;
@@ -705,16 +777,23 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
   }
   int CS = 2;
   const bool tr = t.trace != nullptr;
-  if (tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr).total > kSmemMax) CS = 1;
-  const size_t smem = tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr).total;
+  if (tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr, t.SS).total > kSmemMax) CS = 1;
+  const size_t smem = tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr, t.SS).total;
   if (smem > kSmemMax) { g_tc_msg = "shared memory budget (codes rows too wide)"; return ITLUMM_EUNSUPPORTED; }
   TcpKArgs k{};
   k.codes = a.codes; k.ldc = a.ldc; k.N = a.N; k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo;
-  k.relu = a.relu; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.ST = t.ST; k.CS = CS; k.tmem_cols = t.tmem_cols;
+  k.relu = a.relu; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.ST = t.ST; k.SS = t.SS; k.CS = CS; k.tmem_cols = t.tmem_cols;
   k.pdl = pdl ? 1 : 0;
   k.trace = t.trace;
   static const int dbg = getenv("ITLUMM_TCP_DBG") ? atoi(getenv("ITLUMM_TCP_DBG")) : 0;   // developer
   k.dbg = dbg;
+  static const int grp = getenv("ITLUMM_TCP_GROUP") ? atoi(getenv("ITLUMM_TCP_GROUP")) : 0;   // developer
+  k.group = grp < 0 ? 0 : grp > 4 ? 4 : grp;
+  static const int pbar = getenv("ITLUMM_TCP_PBAR") ? atoi(getenv("ITLUMM_TCP_PBAR")) : 0;   // developer
+  k.pbar = pbar;
+  static const int cl_env = getenv("ITLUMM_TCP_CLOAD") ? atoi(getenv("ITLUMM_TCP_CLOAD")) : 1;   // developer
+  k.cload = cl_env;
+  if (k.group > t.ST) k.group = t.ST;
   const int64_t units = ((a.N + 255) / 256) * t.G;
   const void* kfn = t.mode == kTcpSel ? (const void*)k_tcp<kTcpSel>
                   : t.mode == kTcpSparse ? (const void*)k_tcp<kTcpSparse> : (const void*)k_tcp<kTcpDense>;
