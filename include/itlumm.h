@@ -83,19 +83,14 @@ typedef enum {
 typedef enum { ITLUMM_SUM_EXACT = 0, ITLUMM_SUM_AVG16 = 1 } itlumm_summation;
 
 /* Operand form of the one-hot matrix G on the tensor-core paths (TC, TC_PIPE).
- *   AUTO     : library choice: SELECT for a LUT streamed through shared memory (large C x M),
- *              DENSE for a resident one.
+ *   AUTO     : library choice: DENSE (measured fastest on every kernel).
  *   DENSE    : G as u8 (16 bytes per codebook), tcgen05.mma kind::i8, K = 32 per instruction.
  *   SPARSE24 : G is 1-of-16 per codebook, hence 2:4 sparse: stored compressed (8 bytes per
  *              codebook) with 2-bit position metadata per stored element, tcgen05.mma.sp kind::i8,
  *              K = 64 per instruction; N slices of at most 224 columns (TMEM holds the metadata).
- *   SELECT   : G moves into the 2:4 sparsity metadata: a constant A operand (values 0, 1 per
- *              group of 4) and a LUT image with one zero row and 3 entries per group of 4 K rows
- *              (24 K per codebook), so the metadata of a row selects LUT rows (CTA-pair kernel,
- *              any shape; N slices of at most 224 columns).
  * All give the same exact integer products (bit-identical results). */
 typedef enum {
-  ITLUMM_ONEHOT_AUTO = 0, ITLUMM_ONEHOT_DENSE = 1, ITLUMM_ONEHOT_SPARSE24 = 2, ITLUMM_ONEHOT_SELECT = 3
+  ITLUMM_ONEHOT_AUTO = 0, ITLUMM_ONEHOT_DENSE = 1, ITLUMM_ONEHOT_SPARSE24 = 2
 } itlumm_onehot;
 
 typedef struct itlumm_plan_s* itlumm_plan; /* opaque; owns device copies of all parameters */

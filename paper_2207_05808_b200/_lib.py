@@ -15,7 +15,7 @@ F32, BF16 = 0, 1
 EPI_NONE, EPI_RELU = 0, 1
 ALGO = {"auto": 0, "simt": 1, "tc": 2, "tc_pipe": 3}
 SUMMATION = {"exact": 0, "avg16": 1}
-ONEHOT = {"auto": 0, "dense": 1, "sparse24": 2, "select": 3}
+ONEHOT = {"auto": 0, "dense": 1, "sparse24": 2}
 
 # every symbol include/itlumm.h declares (checked by tests/test_abi.py against the header)
 EXPORTS = [

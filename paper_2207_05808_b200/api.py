@@ -115,10 +115,9 @@ class Plan:
         self.summation = summation
 
     def set_onehot(self, onehot: str):
-        """"auto" (default: the library's choice), "dense", "sparse24" or "select": the one-hot
-        operand of the tensor-core paths (tcgen05.mma.sp for the 2:4-sparse form; the
-        one-hot as sparsity metadata over a constant A for "select", include/itlumm.h);
-        bit-identical results."""
+        """"auto" (default: the library's choice), "dense" or "sparse24": the one-hot operand of
+        the tensor-core paths (tcgen05.mma.sp for the 2:4-sparse form); bit-identical
+        results."""
         _lib.check(self._lib.itlumm_plan_set_onehot(self._h, _lib.ONEHOT[onehot]))
         self.onehot = onehot
 

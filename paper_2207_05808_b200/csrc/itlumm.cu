@@ -64,7 +64,6 @@ struct itlumm_plan_s {
   itlumm_onehot onehot = ITLUMM_ONEHOT_AUTO;
   TcpPlan pair_sp{};             // CTA-pair kernel over the sparse tiling (streamed LUT), AUTO's choice
   TcpPlan pair_dn{};             // the same over the dense tiling
-  TcpPlan pair_sel{};            // CTA-pair kernel in selector mode (one-hot as sparsity metadata)
   // TC_PIPE code scratch (allocated at plan creation; reuse ordered by scratch_ev)
   std::mutex scratch_mu;
   uint8_t* scratch = nullptr;
@@ -264,13 +263,10 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
     for (int h = 0; h < 15; ++h) thr_t[(size_t)h * C + c] = p->thresholds[c * 15 + h];
   std::vector<uint8_t> lut((size_t)C * 16 * Mp, 0);
   for (size_t r = 0; r < (size_t)C * 16; ++r) memcpy(&lut[r * Mp], p->lut + r * M, M);
-  std::vector<uint8_t> qt, qs, qz;
+  std::vector<uint8_t> qt, qs;
   tc_layout_host(C, M, p->lut, &P->tc, qt);
   tc_layout_host(C, M, p->lut, &P->tcs, qs, true);
-  int sel_ns = 0, sel_g = 0, sel_kb = 0;
-  if (P->tc.ok && !sel_layout_host(C, M, p->lut, sel_ns, sel_g, sel_kb, qz)) qz.clear();
-  const int Mpad = std::max({Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0, P->tcs.ok ? P->tcs.G * P->tcs.NS : 0,
-                             qz.empty() ? 0 : sel_g * sel_ns});   // slice columns past M read 0
+  const int Mpad = std::max({Mp, P->tc.ok ? P->tc.G * P->tc.NS : 0, P->tcs.ok ? P->tcs.G * P->tcs.NS : 0});   // slice columns past M read 0
   std::vector<float> scale(Mpad, 0.f), offtot(Mpad, 0.f), offavg(Mpad, 0.f);
   for (int m = 0; m < M; ++m) {
     scale[m] = p->scale[m];
@@ -285,8 +281,8 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t o_cols = 0, o_thr = o_cols + al(cols.size() * 4), o_lut = o_thr + al(thr_t.size() * 4),
                o_sc = o_lut + al(lut.size()), o_ot = o_sc + al((size_t)Mpad * 4), o_oa = o_ot + al((size_t)Mpad * 4),
-               o_qt = o_oa + al((size_t)Mpad * 4), o_qs = o_qt + al(qt.size()), o_qz = o_qs + al(qs.size()),
-               total = o_qz + al(qz.size());
+               o_qt = o_oa + al((size_t)Mpad * 4), o_qs = o_qt + al(qt.size()),
+               total = o_qs + al(qs.size());
   int prev = 0;
   cudaGetDevice(&prev);
   auto cleanup = [&](itlumm_status st) {
@@ -307,8 +303,7 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
       {o_cols, cols.data(), cols.size() * 4}, {o_thr, thr_t.data(), thr_t.size() * 4},
       {o_lut, lut.data(), lut.size()},        {o_sc, scale.data(), (size_t)Mpad * 4},
       {o_ot, offtot.data(), (size_t)Mpad * 4},  {o_oa, offavg.data(), (size_t)Mpad * 4},
-      {o_qt, qt.data(), qt.size()},           {o_qs, qs.data(), qs.size()},
-      {o_qz, qz.data(), qz.size()}};
+      {o_qt, qt.data(), qt.size()},           {o_qs, qs.data(), qs.size()}};
   for (auto& c : cp) {
     if (!c.n) continue;
     e = cudaMemcpy(base + c.off, c.src, c.n, cudaMemcpyHostToDevice);
@@ -339,8 +334,7 @@ static itlumm_status plan_create_impl(const itlumm_params* p0, int cuda_device, 
   if (st != ITLUMM_OK) return cleanup(fail(st, "%s", tc_last_msg()));
   if (P->tcs.ok && P->tcs.stream_b) tcp_configure(P->pair_sp, P->tcs, P->num_sms);
   if (P->tc.ok && P->tc.stream_b) tcp_configure(P->pair_dn, P->tc, P->num_sms);
-  if (!qz.empty()) tcp_configure_sel(P->pair_sel, C, sel_ns, sel_g, sel_kb, base + o_qz, P->num_sms);
-  P->pair_sp.trace = P->pair_dn.trace = P->pair_sel.trace = P->tc.trace;
+  P->pair_sp.trace = P->pair_dn.trace = P->tc.trace;
   if (P->tc.ok || P->tcs.ok) {
     P->scratch_ldc = (((C + 1) / 2) + 15) & ~15;
     P->scratch_rows = 262144;
@@ -400,12 +394,10 @@ extern "C" itlumm_status itlumm_plan_set_summation(itlumm_plan P, itlumm_summati
 extern "C" itlumm_status itlumm_plan_set_onehot(itlumm_plan P, itlumm_onehot o) {
   g_err.clear();
   if (!P) return fail(ITLUMM_EINVAL, "plan is NULL");
-  if (o != ITLUMM_ONEHOT_AUTO && o != ITLUMM_ONEHOT_DENSE && o != ITLUMM_ONEHOT_SPARSE24 && o != ITLUMM_ONEHOT_SELECT)
+  if (o != ITLUMM_ONEHOT_AUTO && o != ITLUMM_ONEHOT_DENSE && o != ITLUMM_ONEHOT_SPARSE24)
     return fail(ITLUMM_EINVAL, "bad onehot %d", (int)o);
   if (o == ITLUMM_ONEHOT_SPARSE24 && !P->tcs.ok)
     return fail(ITLUMM_EUNSUPPORTED, "2:4-sparse one-hot tiling unsupported for this plan: %s", P->tcs.why);
-  if (o == ITLUMM_ONEHOT_SELECT && !P->pair_sel.ok)
-    return fail(ITLUMM_EUNSUPPORTED, "selector tiling unsupported for this plan: %s", P->pair_sel.why);
   P->onehot = o;
   return ITLUMM_OK;
 }
@@ -566,22 +558,15 @@ extern "C" itlumm_status itlumm_encode(itlumm_plan P, const void* A, itlumm_dtyp
   return launch_encode(P, A, dtype, lda, N, codes, ldc, (cudaStream_t)stream);
 }
 
-// The 1-CTA tensor-core tiling in use: dense (AUTO, DENSE, SELECT) or 2:4-sparse one-hot (SPARSE24).
+// The 1-CTA tensor-core tiling in use: dense (AUTO, DENSE) or 2:4-sparse one-hot (SPARSE24).
 static const TcPlan& tcp(itlumm_plan P) { return P->onehot == ITLUMM_ONEHOT_SPARSE24 ? P->tcs : P->tc; }
 
-// Tensor-core accumulate of codes (a3' + a4).  SELECT runs the CTA-pair kernel in selector mode on
-// any shape; under AUTO a streamed LUT runs the pair kernel in selector mode, or
-// with the one-hot operand DENSE / SPARSE24 when asked; a resident LUT runs the 1-CTA k_tc.
-// Developer knob (not ABI): ITLUMM_PAIR=0 keeps streamed LUTs on k_tc.
+// Tensor-core accumulate of codes (a3' + a4): a streamed LUT runs the CTA-pair kernel k_tcp (dense
+// or 2:4-sparse one-hot), a resident LUT the 1-CTA k_tc.  Developer knob (not ABI): ITLUMM_PAIR=0
+// keeps streamed LUTs on k_tc.
 static itlumm_status launch_tc_acc(itlumm_plan P, const TcArgs& a, cudaStream_t s, bool pdl) {
   static const bool pair_on = !(getenv("ITLUMM_PAIR") && atoi(getenv("ITLUMM_PAIR")) == 0);
-  static const bool sel_auto = getenv("ITLUMM_SEL") && atoi(getenv("ITLUMM_SEL")) != 0;   // developer
   const TcPlan& t = tcp(P);
-  if (P->onehot == ITLUMM_ONEHOT_SELECT ||
-      (pair_on && sel_auto && P->onehot == ITLUMM_ONEHOT_AUTO && t.ok && t.stream_b && P->pair_sel.ok)) {
-    const itlumm_status st = tcp_launch(P->pair_sel, P->dp, a, s, pdl);
-    if (st != ITLUMM_EUNSUPPORTED) return st;   // codes rows the pair kernel cannot take: k_tc below
-  }
   if (pair_on && t.ok && t.stream_b) {
     const TcpPlan& pp = P->onehot == ITLUMM_ONEHOT_SPARSE24 ? P->pair_sp : P->pair_dn;
     if (pp.ok) {

@@ -26,32 +26,12 @@
 //   warp 13     loader: the CTA's 128-row codes tile (bulk copy) and its half of each LUT K-block
 //               (TMA tensor load .cta_group::2: the bytes complete on the LEADER's full[st]).
 // Results are bit-identical to every other schedule (exact integer MMA, the same single fmaf).
-//
-// SELECTOR mode (MODE = kTcpSel): the one-hot moves into the sparsity metadata and the A operand
-// becomes a constant.  A 2:4-sparse MMA computes, per group of 4 K-positions, v0 * B[idx0] +
-// v1 * B[idx1] with the group's two stored A values (v0, v1) and the 2-bit indices of its metadata
-// nibble.  With A = (0, 1) in every group (one constant 8 KB tile, never rewritten) a group
-// contributes B[idx1]: the metadata SELECTS a LUT row.  The LUT image gives each group one zero row
-// (position 0: idx1 = 0 contributes nothing) and three LUT entries (positions 1..3), so a codebook
-// takes 6 groups = 24 K-positions (entry j at 4 (j / 3) + 1 + j % 3; 16 entries + 2 unused zero
-// slots), and row r's codebook-c contribution is lut[c][code][.] exactly as G.Q's.
-// The producers write 3 bytes of metadata per (row, codebook) instead of a 16-byte one-hot chunk,
-// and the MMA does 24 K per codebook at the sparse rate (2x dense per K on a pair): 0.75x the
-// dense one-hot's MMA time, for a 1.5x larger LUT image (the L2 -> shared-memory stream).
 #pragma once
 #include "tc.cuh"
 
 namespace itlumm {
 
-constexpr int kTcpDense = 0, kTcpSparse = 1, kTcpSel = 2;   // k_tcp MODE
-constexpr int kSelK = 24;               // K-positions per codebook in the selector image
-constexpr int kSelBlk = 64;             // bytes (= K) per SW64 B block: one sparse K=64 MMA
-constexpr int kSelBlocks = 3;           // blocks per ring stage: 8 codebooks x 24 = 192 K
-constexpr int kSelMeta = 2 * kTcRows * 16;   // per stage: two 128-row x 16 B tcgen05.cp sources
-constexpr int kSelMetaCols = 8;         // TMEM metadata columns per stage (6 used)
-constexpr int kSelNsMax = 224;          // 2 x NS accumulators + 8 metadata columns per stage <= 512
-// K index, within its codebook's 24, of LUT entry j (group j / 3, position 1 + j % 3)
-__host__ __device__ constexpr int sel_kpos(int j) { return 4 * (j / 3) + 1 + j % 3; }
+constexpr int kTcpDense = 0, kTcpSparse = 1;   // k_tcp MODE
 
 // Roles: 8 producer warps (two threads per row, four codebooks each), 1 MMA warp, 8 epilogue warps
 // (two per TMEM lane quadrant), 1 loader warp.  Two threads per row: one producer warp per SM
@@ -105,14 +85,6 @@ __device__ __forceinline__ void onehot_sparse8(uint32_t k, uint32_t& lo, uint32_
   hi = (uint32_t)(v >> 32);
   m16 = (((k & 3u) ^ (t * 3u)) | 12u) << (k & 12u);
   if (k >= 16u) m16 = 0u;
-}
-// Selector mode: one codebook's 6 metadata nibbles (24 bits) for code k (k >= 16: none).  Nibble g
-// = idx0 | idx1 << 2 with idx0 = 0 (value 0) and idx1 = 1 + k % 3 in the group g = k / 3 that holds
-// entry k, idx1 = 0 (the zero row) in the other five.
-__device__ __forceinline__ uint32_t sel_field(uint32_t k) {
-  const uint32_t q = (k * 11u) >> 5;     // k / 3 for k < 16
-  const uint32_t rem = k - 3u * q;
-  return k < 16u ? (rem + 1u) << (4u * q + 2u) : 0u;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -176,23 +148,21 @@ __host__ __device__ constexpr uint32_t idesc_i8_m256(int n) {
   return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
-// Per-CTA shared memory: ST ring stages of [A | metadata | B half], CS codes tiles, epilogue staging.
-// Selector mode: no per-stage A (the constant A tile sits after the ring), 2 x 2 KB of metadata
-// and three SW64 B blocks of NS/2 rows x 64 B.
+// Per-CTA shared memory: ST ring slots of SS stages [A | metadata | B half], CS codes tiles (0: the
+// codes come straight from global memory), epilogue staging.
 struct TcpSmem {
-  size_t a_bytes, e_bytes, b_bytes, stage, ring, aconst, codes, stg, bar, tmem, trc, total;
+  size_t a_bytes, e_bytes, b_bytes, stage, ring, codes, stg, bar, tmem, trc, total;
 };
-constexpr int kTcpTrcSlots = 16, kTcpTrcWin = 64, kTcpTrcFirst = 96;   // developer timeline window
+constexpr int kTcpTrcSlots = 24, kTcpTrcWin = 64, kTcpTrcFirst = 96;   // developer timeline window
 __host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int CS, int ldc, bool trace = false, int SS = 1) {
   TcpSmem s{};
-  const bool sp = mode == kTcpSparse, sel = mode == kTcpSel;
-  s.a_bytes = sel ? 0 : sp ? (size_t)kSpA : (size_t)kTcRows * kKBlock;          // 8 KB compressed / 16 KB dense
-  s.e_bytes = sel ? (size_t)kSelMeta : sp ? (size_t)kTcRows * 16 : 0;           // metadata rows (tcgen05.cp source)
-  s.b_bytes = sel ? (size_t)kSelBlocks * (NS / 2) * kSelBlk : (size_t)(NS / 2) * kKBlock;   // half a LUT K-block
+  const bool sp = mode == kTcpSparse;
+  s.a_bytes = sp ? (size_t)kSpA : (size_t)kTcRows * kKBlock;          // 8 KB compressed / 16 KB dense
+  s.e_bytes = sp ? (size_t)kTcRows * 16 : 0;                         // metadata rows (tcgen05.cp source)
+  s.b_bytes = (size_t)(NS / 2) * kKBlock;                            // half a LUT K-block
   s.stage = (s.a_bytes + s.e_bytes + s.b_bytes + 1023) & ~(size_t)1023;
   s.ring = 0;
-  s.aconst = s.ring + (size_t)ST * SS * s.stage;   // ST ring slots of SS sub-stages (one K-block each)
-  s.codes = s.aconst + (sel ? (size_t)kSpA : 0);
+  s.codes = s.ring + (size_t)ST * SS * s.stage;   // ST ring slots of SS sub-stages (one K-block each)
   s.stg = s.codes + (((size_t)CS * kTcRows * ldc + 1023) & ~(size_t)1023);
   s.bar = s.stg + (size_t)kTcEpiWarps * kTcStage;
   s.tmem = s.bar + (size_t)(2 * ST + 4 + 2 * CS) * 8;
@@ -213,8 +183,6 @@ struct TcpKArgs {
   int pdl;
   uint64_t* trace;                     // developer timeline (ITLUMM_TC_TRACE=1): [4 CTAs][4 roles][kTraceEv]
   int cload;                           // codes tiles loaded by their own warp (16) instead of the LUT loader
-  int pbar;                            // producers arrive once per CTA (named barrier) instead of per warp
-  int group;                           // MMA issue: stages per pass (1-4), 0 = adaptive (test_wait probe)
   int dbg;                             // developer removal switches (ITLUMM_TCP_DBG; results then wrong):
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
@@ -226,19 +194,12 @@ struct TcpKArgs {
 template <int MODE>
 __global__ void __launch_bounds__(kTcpThreads, 1)
 k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap qt_map) {
-  constexpr bool SP = MODE == kTcpSparse, SEL = MODE == kTcpSel;
+  constexpr bool SP = MODE == kTcpSparse;
   extern __shared__ __align__(1024) uint8_t smem_tcp[];
   uint8_t* smem = smem_tcp + ((1024u - (smem_u32(smem_tcp) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, ST = g.ST, CS = g.CS, SS = g.SS;
   const int KBS = KB / SS;                 // ring slots per item
   const TcpSmem L = tcp_smem_layout(MODE, NS, ST, CS, (int)g.ldc, g.trace != nullptr, SS);
-  // MMA width of slice sl: selector slices are NS wide except a narrower last one (whole 32-column
-  // epilogue chunks), so that a 4096-column layer in 224-column slices runs no padding columns
-  auto slice_n = [&](int sl) -> int {
-    if (!SEL) return NS;
-    const int w = (p.M - sl * NS + 31) / 32 * 32;
-    return w < NS ? w : NS;
-  };
   uint8_t* ring = smem + L.ring;
   uint8_t* codes_s = smem + L.codes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar);   // leader: 8 producer warps + loader tx
@@ -263,6 +224,15 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     if (g.trace && blockIdx.x < 2 && slot < kTcpTrcSlots && i >= kTcpTrcFirst && i < kTcpTrcFirst + kTcpTrcWin)
       trc[slot * kTcpTrcWin + (i - kTcpTrcFirst)] = clock64();   // SM cycles (cheap; %globaltimer reads are not)
   };
+  // slots 16..: %globaltimer (ns, comparable across the pair's two SMs): 16 MMA full-wait done,
+  // 17 / 19 producer role 0 / 7 arrived, 18 LUT loader issued (each CTA its own)
+  auto stampg = [&](int slot, int64_t i) {
+    if (g.trace && blockIdx.x < 2 && i >= kTcpTrcFirst && i < kTcpTrcFirst + kTcpTrcWin) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trc[slot * kTcpTrcWin + (i - kTcpTrcFirst)] = t;
+    }
+  };
   const int64_t ntiles = (g.N + 2 * kTcRows - 1) / (2 * kTcRows);    // 256-row pair tiles
   const int64_t units = ntiles * G;
   // k-th item of this pair: u = pair + k * npair; consecutive pairs share a slice (its LUT K-blocks
@@ -276,15 +246,12 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, (g.pbar ? 2 : 2 * kTcpProdWarps) + 1); mbar_init(empty_bar + s, 1); }
+    // developer: 16384 takes the producers out of the ring, 32768 the LUT loader (timing only)
+    const int nfull = ((g.dbg & 16384) ? 0 : 2 * kTcpProdWarps) + ((g.dbg & 32768) ? 0 : 1);
+    for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, nfull); mbar_init(empty_bar + s, 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, 2 * kTcpEpiWarps); }
     for (int s = 0; s < CS; ++s) { mbar_init(codes_full + s, 1); mbar_init(codes_empty + s, kTcpProdWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (SEL) {   // the constant compressed A: values (v0, v1) = (0, 1) in every group, all 128 rows
-    uint32_t* a = reinterpret_cast<uint32_t*>(smem + L.aconst);
-    for (int i = threadIdx.x; i < kSpA / 4; i += blockDim.x) a[i] = 0x01000100u;
-    fence_proxy_async_smem();
   }
   if (warp == kTcpLoaderWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qt_map)) : "memory");
@@ -316,7 +283,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       mbar_arrive(codes_full + cs);                    // a pair tile's empty second half
     }
   };
-  if (g.cload && role == 18) {
+  if (g.cload && CS > 0 && role == 18) {
     // ================================================================ codes loader (own warp): up to
     // CS items ahead of the producers, independent of the LUT ring (the LUT loader runs only ST
     // slots ahead of the MMAs, too late to hide a codes tile's L2/HBM latency at an item boundary)
@@ -333,33 +300,25 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     }
   } else if (warp == kTcpLoaderWarp) {
     // ================================================================ loader (one lane per CTA)
-    if (lane == 0) {
+    if (lane == 0 && !(g.dbg & 32768)) {
       const uint32_t bhalf = (uint32_t)(NS / 2) * kKBlock;
       int cs = 0, st = 0;
       uint32_t cph = 0, ph = 0;
       int64_t tile;
       int sl;
       for (int64_t k = 0; item(k, tile, sl); ++k) {
-        if (!g.cload) {
+        if (!g.cload && CS > 0) {
           mbar_wait(codes_empty + cs, cph ^ 1);
           load_codes(tile, cs);
           if (++cs == CS) { cs = 0; cph ^= 1; }
         }
         const int y0 = (sl * KB) * NS + (int)rank * (NS / 2);
-        // selector image: [G][3 KB][NS rows][64 B]; this CTA's rows of a block start at rank * n / 2
-        const int ys = (sl * KB * kSelBlocks) * NS + (int)rank * (slice_n(sl) / 2);
-        const uint32_t sbox = (uint32_t)(NS / 2) * kSelBlk;
         for (int kb = 0; kb < KBS; ++kb) {
           mbar_wait(empty_bar + st, ph ^ 1);  // the pair's MMAs are done with the slot
           stamp(2 + (int)rank, k * KBS + kb);
+          stampg(18, k * KBS + kb);
           if (g.dbg & 4) {
             if (rank == 0) mbar_arrive(full_bar + st);
-          } else if (SEL) {
-            if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * kSelBlocks * sbox);
-            uint8_t* bs = ring + (size_t)st * L.stage + L.e_bytes;
-#pragma unroll
-            for (int j = 0; j < kSelBlocks; ++j)
-              tma_load_2d_pair(bs + j * sbox, &qt_map, 0, ys + (kb * kSelBlocks + j) * NS, full_leader + 8u * st);
           } else {
             if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * bhalf * SS);
             for (int j = 0; j < SS; ++j)
@@ -383,12 +342,38 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     uint32_t doff[4];                                    // this thread's 16-byte chunks (dense layout)
 #pragma unroll
     for (int j = 0; j < 4; ++j) doff[j] = sw128_off(r, 4 * half + j);
+    // CS == 0: no codes tiles in shared memory (that space deepens the ring); each thread loads its
+    // row's codes from global memory, 16 B per 4 K-blocks, one load ahead (across items too)
+    const bool cdir = CS == 0;
+    auto grow = [&](int64_t t) -> const uint8_t* {
+      const int64_t rw = t * 2 * kTcRows + (int64_t)rank * kTcRows + r;
+      return rw < g.N ? g.codes + rw * g.ldc : nullptr;
+    };
+    uint4 qnext = make_uint4(0, 0, 0, 0);
+    if (cdir && item(0, tile, sl)) {
+      const uint8_t* g0 = grow(tile);
+      if (g0) qnext = __ldg(reinterpret_cast<const uint4*>(g0));
+    }
     for (int64_t k = 0; item(k, tile, sl); ++k) {
-      mbar_wait(codes_full + cs, cph);
+      if (!cdir) mbar_wait(codes_full + cs, cph);
       const int64_t row = tile * 2 * kTcRows + (int64_t)rank * kTcRows + r;
       const bool valid = row < g.N;
-      const uint8_t* crow = codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
+      const uint8_t* crow = cdir ? grow(tile) : codes_s + ((size_t)cs * kTcRows + r) * g.ldc;
+      const uint8_t* cnext = nullptr;                  // the next item's codes row (prefetch)
+      if (cdir) {
+        int64_t t2;
+        int s2;
+        if (item(k + 1, t2, s2)) cnext = grow(t2);
+      }
       uint4 quad = make_uint4(0, 0, 0, 0);
+      if (g.dbg & 16384) {
+        __syncwarp();
+        if (!cdir) {
+          if (lane == 0) mbar_arrive(codes_empty + cs);
+          if (++cs == CS) { cs = 0; cph ^= 1; }
+        }
+        continue;
+      }
       // one ring stage per proxy fence and arrive: pairing stages made a stage wait for the NEXT
       // stage's slot to free up (one MMA pass later), which cost more than the fence it saved
       for (int kb = 0; kb < KBS; ++kb) {
@@ -396,7 +381,15 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         for (int jj = 0; jj < 2; ++jj) {
           if (jj >= SS) break;
           const int kbi = kb * SS + jj;
-          if ((kbi & 3) == 0 && valid) quad = *reinterpret_cast<const uint4*>(crow + kbi * 4);   // 4 K-blocks of codes
+          if ((kbi & 3) == 0) {                          // 4 K-blocks of codes
+            if (cdir) {
+              quad = qnext;
+              const uint8_t* src = kbi + 4 < KB ? (valid ? crow + (kbi + 4) * 4 : nullptr) : cnext;
+              if (src) qnext = __ldg(reinterpret_cast<const uint4*>(src));
+            } else if (valid) {
+              quad = *reinterpret_cast<const uint4*>(crow + kbi * 4);
+            }
+          }
           const uint32_t cw = ((kbi & 3) == 0 ? quad.x : (kbi & 3) == 1 ? quad.y : (kbi & 3) == 2 ? quad.z : quad.w) >> (16 * half);
           const int c0 = kbi * 8 + 4 * half;               // first codebook of this thread
           const int nv = valid ? (C - c0 < 0 ? 0 : (C - c0 > 4 ? 4 : C - c0)) : 0;
@@ -407,19 +400,6 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
 
           uint8_t* stg_a = ring + (size_t)(st * SS + jj) * L.stage;
           if (g.dbg & 1) {
-          } else if (SEL) {
-            // 96 metadata bits of codebooks 4 half .. +3 at bits 96 half .. of the row's 192; bytes
-            // 0-15 are the first tcgen05.cp source (MMAs 0, 1), bytes 16-23 the second (MMA 2)
-            const uint32_t f0 = sel_field(code[0]), f1 = sel_field(code[1]), f2 = sel_field(code[2]),
-                           f3 = sel_field(code[3]);
-            const uint32_t w0 = f0 | (f1 << 24), w1 = (f1 >> 8) | (f2 << 16), w2 = (f2 >> 16) | (f3 << 8);
-            if (half == 0) {
-              *reinterpret_cast<uint2*>(stg_a + 16 * r) = make_uint2(w0, w1);
-              *reinterpret_cast<uint32_t*>(stg_a + 16 * r + 8) = w2;
-            } else {
-              *reinterpret_cast<uint32_t*>(stg_a + 16 * r + 12) = w0;
-              *reinterpret_cast<uint2*>(stg_a + kTcRows * 16 + 16 * r) = make_uint2(w1, w2);
-            }
           } else if (SP) {
             uint32_t lo[4], hi[4], m[4];
 #pragma unroll
@@ -444,20 +424,17 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           }
         }
         if (!(g.dbg & 8)) fence_proxy_async_smem();
-        if (g.pbar) {
-          // one arrival per CTA: the 8 producer warps meet at a named barrier first
-          asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcpProdWarps) : "memory");
-          if (role == 0 && lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
-        } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
         if (lane == 0 && rank == 0) stamp(4 + role, k * KBS + kb);
+        if (lane == 0 && (role == 0 || role == 7)) stampg(role == 0 ? 17 : 19, k * KBS + kb);
         if (++st == ST) { st = 0; ph ^= 1; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(codes_empty + cs);
-      if (++cs == CS) { cs = 0; cph ^= 1; }
+      if (!cdir) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(codes_empty + cs);
+        if (++cs == CS) { cs = 0; cph ^= 1; }
+      }
     }
   } else if (warp == kTcpMmaWarp) {
     // ================================================================ MMA issuer (leader warp)
@@ -465,13 +442,11 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     // elected lane issues each tcgen05 op: a lone lane == 0 thread made the compiler move every
     // descriptor through R2UR and wrap each op in an elect loop (~190 ns per stage, tcp_trace).
     if (rank == 0) {
-      uint32_t idesc = idesc_i8_m256(NS);
+      const uint32_t idesc = idesc_i8_m256(NS);
       const uint32_t r0 = smem_u32(ring);
-      const uint64_t a_desc0 = SEL ? umma_desc_sw64(smem_u32(smem + L.aconst)) : SP ? umma_desc_sw64(r0) : umma_desc_sw128(r0);
+      const uint64_t a_desc0 = SP ? umma_desc_sw64(r0) : umma_desc_sw128(r0);
       const uint64_t e_desc0 = umma_desc_rows16(r0 + (uint32_t)L.a_bytes);
-      const uint64_t b_desc0 = SEL ? umma_desc_sw64(r0 + (uint32_t)L.e_bytes)
-                                   : umma_desc_sw128(r0 + (uint32_t)(L.a_bytes + L.e_bytes));
-      const uint32_t sblk = (uint32_t)((NS / 2) * kSelBlk) >> 4;   // selector: B block stride (16 B units)
+      const uint64_t b_desc0 = umma_desc_sw128(r0 + (uint32_t)(L.a_bytes + L.e_bytes));
       const uint32_t step = (uint32_t)(L.stage >> 4);
       const uint32_t e_col0 = tmem_base + (uint32_t)(2 * NS);
       int st = 0, acc = 0;
@@ -487,17 +462,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         const uint64_t ad = a_desc0 + (uint64_t)(stg * step);
         const uint64_t bd = b_desc0 + (uint64_t)(stg * step);
         if (g.dbg & 2) return;
-        if (SEL) {
-          // metadata of both CTAs' 128 rows to TMEM, then 3 K=64 sparse MMAs over the constant A;
-          // tcgen05.cp and tcgen05.mma from this thread execute in issue order
-          const uint32_t e = e_col0 + (uint32_t)(kSelMetaCols * stg);
-          const uint64_t md = e_desc0 + (uint64_t)(stg * step);
-          tmem_cp_pair_128x128b(e, md);
-          tmem_cp_pair_128x128b(e + 4, md + (uint64_t)((kTcRows * 16) >> 4));
-          umma_sp_i8_pair(d, a_desc0, bd, e, idesc, kb != 0);
-          umma_sp_i8_pair(d, a_desc0, bd + sblk, e + 2, idesc, 1u);
-          umma_sp_i8_pair(d, a_desc0, bd + 2 * sblk, e + 4, idesc, 1u);
-        } else if (SP) {
+        if (SP) {
           const uint32_t e = e_col0 + 4u * stg;
           tmem_cp_pair_128x128b(e, e_desc0 + (uint64_t)(stg * step));
           umma_sp_i8_pair(d, ad, bd, e, idesc, kb != 0);            // K = 64: codebooks 0-3
@@ -517,39 +482,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       for (int64_t k = 0; item(k, tile, sl); ++k) {
         mbar_wait(acce_bar + acc, aph ^ 1);   // both CTAs' epilogues drained this accumulator
         tc_fence_after();
-        if (SEL) idesc = idesc_i8_m256(slice_n(sl));
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
-        if (g.group > 0) {
-          // fixed groups of g.group stages per pass: wait for each (already-complete try_wait ~90
-          // cycles), then issue them all; no test_wait probe (~150 cycles) of the next stage
-          for (int kb = 0; kb < KBS;) {
-            const int np = KBS - kb < g.group ? KBS - kb : g.group;
-            int sts[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              sts[i] = st;
-              if (i < np) {
-                mbar_wait(full_bar + st, ph);
-                if (++st == ST) { st = 0; ph ^= 1; }
-              }
-            }
-            if (lane == 0) stamp(0, k * KBS + kb);
-            if (elect_one()) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (i < np) issue_slot(sts[i], kb + i, d);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (i < np) umma_commit_pair(empty_bar + sts[i]);
-              if (kb + np >= KBS) umma_commit_pair(accf_bar + acc);
-            }
-            __syncwarp();
-            if (lane == 0) stamp(1, k * KBS + kb);
-            kb += np;
-          }
-          if (++acc == 2) { acc = 0; aph ^= 1; }
-          continue;
-        }
         for (int kb = 0; kb < KBS;) {
           const int st1 = st + 1 == ST ? 0 : st + 1;
           const uint32_t ph1 = st + 1 == ST ? ph ^ 1 : ph;
@@ -558,11 +491,21 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           const bool two = !(g.dbg & 4096) &&
                            __shfl_sync(0xffffffffu, (int)(kb + 1 < KBS && mbar_test(full_bar + st1, ph1)), 0) != 0;
           if (lane == 0) stamp(0, k * KBS + kb);
+          if (lane == 0) stampg(16, k * KBS + kb);
           if (elect_one()) {
             issue_slot(st, kb, d);
             if (two) issue_slot(st1, kb + 1, d);
-            umma_commit_pair(empty_bar + st);
-            if (two) umma_commit_pair(empty_bar + st1);
+            if (g.dbg & 8192) {   // developer: free the slot by plain remote arrivals (no tensor-pipe commit)
+              mbar_arrive_cluster(mapa_shared(smem_u32(empty_bar + st), 0));
+              mbar_arrive_cluster(mapa_shared(smem_u32(empty_bar + st), 1));
+              if (two) {
+                mbar_arrive_cluster(mapa_shared(smem_u32(empty_bar + st1), 0));
+                mbar_arrive_cluster(mapa_shared(smem_u32(empty_bar + st1), 1));
+              }
+            } else {
+              umma_commit_pair(empty_bar + st);
+              if (two) umma_commit_pair(empty_bar + st1);
+            }
             if (kb + (two ? 2 : 1) >= KBS) umma_commit_pair(accf_bar + acc);
           }
           __syncwarp();
@@ -592,9 +535,8 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       const int m0 = sl * NS;
       const int64_t row0 = tile * 2 * kTcRows + (int64_t)rank * kTcRows + q * 32;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NS);
-      const int nsl = slice_n(sl);
       if (row0 < g.N && !(g.dbg & 32)) {
-        for (int j0 = h * 32; j0 < nsl; j0 += 64) {
+        for (int j0 = h * 32; j0 < NS; j0 += 64) {
           uint32_t v[32];
           tmem_ld16(tbase + j0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
           tmem_ld16(tbase + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -667,41 +609,12 @@ struct TcpPlan {
   bool ok = false;
   const char* why = "not configured";
   int mode = kTcpDense;
-  int KB = 0, NS = 0, G = 0, ST = 0, SS = 1, tmem_cols = 512;
+  int KB = 0, NS = 0, G = 0, ST = 0, SS = 1, CS = 2, tmem_cols = 512;
   uint64_t* trace = nullptr;
-  const uint8_t* qt = nullptr;         // dense/sparse: [G][KB][NS][128 B] swizzled K-major LUT slices;
-                                       // selector: [G][3 KB][NS][64 B] (sel_layout_host)
+  const uint8_t* qt = nullptr;         // [G][KB][NS][128 B] swizzled K-major LUT slices
   alignas(64) CUtensorMap qt_map;      // 2-D view, one row per (block, column); box = NS/2 rows
   int num_sms = 0;
 };
-
-// Selector image of the uint8 LUT (row-major [C][16][M]): per slice s of NS columns and per 64-K
-// block kz (kz / 3 = ring stage = codebooks 8 (kz / 3) ..), column n's 64 bytes in K-major
-// SWIZZLE_64B order; entry j of codebook c at K = 24 c + sel_kpos(j), every other byte 0.
-// Slices: NS = 224 columns (the TMEM budget: 2 accumulators + metadata), the last one narrower.
-inline bool sel_layout_host(int C, int M, const uint8_t* lut, int& NS, int& G, int& KB, std::vector<uint8_t>& qz) {
-  qz.clear();
-  if (255LL * C >= (1LL << 23)) return false;
-  G = (M + kSelNsMax - 1) / kSelNsMax;
-  NS = kSelNsMax;
-  if (G == 1) NS = (M + 31) / 32 * 32;
-  KB = (C + 7) / 8;
-  const size_t blk = (size_t)NS * kSelBlk;
-  const int KZ = kSelBlocks * KB;
-  qz.assign((size_t)G * KZ * blk, 0);
-  for (int s = 0; s < G; ++s)
-    for (int n = 0; n < NS; ++n) {
-      const int m = s * NS + n;
-      if (m >= M) continue;
-      for (int c = 0; c < C; ++c)
-        for (int j = 0; j < 16; ++j) {
-          const int kk = kSelK * c + sel_kpos(j);
-          const int kz = kk / kSelBlk, kin = kk % kSelBlk;
-          qz[((size_t)s * KZ + kz) * blk + sw64_off(n, kin / 16) + kin % 16] = lut[((size_t)c * 16 + j) * M + m];
-        }
-    }
-  return true;
-}
 
 // Ring depth: as many stages as fit next to 2 codes tiles of the widest rows (ldc up to
 // 16 * ceil(C / 32)) and the epilogue staging, within the TMEM left by the accumulators.
@@ -711,17 +624,19 @@ inline void tcp_finish(TcpPlan& t, int C, int row_bytes) {
   static const int st_env = getenv("ITLUMM_TCP_STAGES") ? atoi(getenv("ITLUMM_TCP_STAGES")) : 0;   // developer
   static const int ss_env = getenv("ITLUMM_TCP_SS") ? atoi(getenv("ITLUMM_TCP_SS")) : 2;   // developer
   t.SS = (t.mode == kTcpDense && ss_env == 2 && t.KB % 2 == 0) ? 2 : 1;
+  static const int cd_env = getenv("ITLUMM_TCP_CDIRECT") ? atoi(getenv("ITLUMM_TCP_CDIRECT")) : 1;   // developer
+  t.CS = cd_env ? 0 : 2;   // 0: codes straight from global memory, the space goes to the ring
   int ST = 12;
-  while (ST > 2 && tcp_smem_layout(t.mode, t.NS, ST, 2, ldc_max, false, t.SS).total > kSmemMax) --ST;
+  while (ST > 2 && tcp_smem_layout(t.mode, t.NS, ST, t.CS, ldc_max, false, t.SS).total > kSmemMax) --ST;
   if (st_env >= 2 && st_env < ST) ST = st_env;
-  const int meta_cols = t.mode == kTcpSel ? kSelMetaCols : t.mode == kTcpSparse ? 4 : 0;
+  const int meta_cols = t.mode == kTcpSparse ? 4 : 0;
   if (meta_cols && 2 * t.NS + meta_cols * ST > 512) ST = (512 - 2 * t.NS) / meta_cols;
   if (ST < 2) { t.why = "shared memory / TMEM budget"; return; }
   t.ST = ST;
   auto enc = tensor_map_encoder();
   if (!enc) { t.why = "no cuTensorMapEncodeTiled"; return; }
   memset(&t.qt_map, 0, sizeof t.qt_map);
-  const int blocks = t.mode == kTcpSel ? kSelBlocks * t.KB : t.KB;
+  const int blocks = t.KB;
   const cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)t.G * blocks * t.NS};
   const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
   const cuuint32_t box[2] = {(cuuint32_t)row_bytes, (cuuint32_t)(t.NS / 2)};
@@ -734,7 +649,6 @@ inline void tcp_finish(TcpPlan& t, int C, int row_bytes) {
   }
   cudaFuncSetAttribute((const void*)k_tcp<kTcpDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   cudaFuncSetAttribute((const void*)k_tcp<kTcpSparse>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-  cudaFuncSetAttribute((const void*)k_tcp<kTcpSel>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   t.ok = true;
   t.why = "";
 }
@@ -749,15 +663,6 @@ inline void tcp_configure(TcpPlan& t, const TcPlan& src, int num_sms) {
   t.mode = src.sp ? kTcpSparse : kTcpDense;
   t.KB = src.KB; t.NS = src.NS; t.G = src.G; t.qt = src.qt; t.num_sms = num_sms;
   tcp_finish(t, src.C, kKBlock);
-}
-
-// The pair kernel in selector mode over the image sel_layout_host built (device copy qz).
-inline void tcp_configure_sel(TcpPlan& t, int C, int NS, int G, int KB, const uint8_t* qz, int num_sms) {
-  t.ok = false;
-  if (!qz) { t.why = "no selector image"; return; }
-  t.mode = kTcpSel;
-  t.KB = KB; t.NS = NS; t.G = G; t.qt = qz; t.num_sms = num_sms;
-  tcp_finish(t, C, kSelBlk);
 }
 
 // Launch on codes (row-major, ldc % 16 == 0, 16-byte aligned base).  Returns EUNSUPPORTED without
@@ -775,9 +680,9 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
     g_tc_msg = "output not TMA-storable (16-byte aligned base and row stride needed)";
     return ITLUMM_EUNSUPPORTED;
   }
-  int CS = 2;
+  int CS = t.CS;
   const bool tr = t.trace != nullptr;
-  if (tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr, t.SS).total > kSmemMax) CS = 1;
+  if (CS > 0 && tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr, t.SS).total > kSmemMax) CS = 1;
   const size_t smem = tcp_smem_layout(t.mode, t.NS, t.ST, CS, (int)a.ldc, tr, t.SS).total;
   if (smem > kSmemMax) { g_tc_msg = "shared memory budget (codes rows too wide)"; return ITLUMM_EUNSUPPORTED; }
   TcpKArgs k{};
@@ -787,16 +692,10 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
   k.trace = t.trace;
   static const int dbg = getenv("ITLUMM_TCP_DBG") ? atoi(getenv("ITLUMM_TCP_DBG")) : 0;   // developer
   k.dbg = dbg;
-  static const int grp = getenv("ITLUMM_TCP_GROUP") ? atoi(getenv("ITLUMM_TCP_GROUP")) : 0;   // developer
-  k.group = grp < 0 ? 0 : grp > 4 ? 4 : grp;
-  static const int pbar = getenv("ITLUMM_TCP_PBAR") ? atoi(getenv("ITLUMM_TCP_PBAR")) : 0;   // developer
-  k.pbar = pbar;
   static const int cl_env = getenv("ITLUMM_TCP_CLOAD") ? atoi(getenv("ITLUMM_TCP_CLOAD")) : 1;   // developer
   k.cload = cl_env;
-  if (k.group > t.ST) k.group = t.ST;
   const int64_t units = ((a.N + 255) / 256) * t.G;
-  const void* kfn = t.mode == kTcpSel ? (const void*)k_tcp<kTcpSel>
-                  : t.mode == kTcpSparse ? (const void*)k_tcp<kTcpSparse> : (const void*)k_tcp<kTcpDense>;
+  const void* kfn = t.mode == kTcpSparse ? (const void*)k_tcp<kTcpSparse> : (const void*)k_tcp<kTcpDense>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kTcpThreads);
   cfg.dynamicSmemBytes = smem;
@@ -822,9 +721,8 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
   if (pairs > units) pairs = units;
   cfg.gridDim = dim3((unsigned)(2 * pairs));
   cfg.numAttrs = pdl ? 2 : 1;
-  cudaError_t e = t.mode == kTcpSel      ? cudaLaunchKernelEx(&cfg, k_tcp<kTcpSel>, dp, k, out_map, t.qt_map)
-                  : t.mode == kTcpSparse ? cudaLaunchKernelEx(&cfg, k_tcp<kTcpSparse>, dp, k, out_map, t.qt_map)
-                                         : cudaLaunchKernelEx(&cfg, k_tcp<kTcpDense>, dp, k, out_map, t.qt_map);
+  cudaError_t e = t.mode == kTcpSparse ? cudaLaunchKernelEx(&cfg, k_tcp<kTcpSparse>, dp, k, out_map, t.qt_map)
+                                       : cudaLaunchKernelEx(&cfg, k_tcp<kTcpDense>, dp, k, out_map, t.qt_map);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }
   return ITLUMM_OK;

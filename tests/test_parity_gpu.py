@@ -15,15 +15,13 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = ATOL = 1e-6
-# "_sp24" / "_dense" / "_sel": the same schedule with the one-hot operand forced to the 2:4-sparse
-# form (tcgen05.mma.sp), the dense form, or the selector form (the one-hot as sparsity
-# metadata over a constant A, CTA-pair kernel on every shape); plain names use the library's choice
-# (AUTO: selector on the CTA-pair streamed-LUT kernel, dense on the 1-CTA kernel)
-ALGOS = ["auto", "simt", "tc", "tc_pipe", "tc_sp24", "tc_pipe_sp24", "tc_pipe_dense", "tc_sel", "tc_pipe_sel"]
+# "_sp24" / "_dense": the same schedule with the one-hot operand forced to the 2:4-sparse form
+# (tcgen05.mma.sp) or the dense form; plain names use the library's choice (AUTO: dense)
+ALGOS = ["auto", "simt", "tc", "tc_pipe", "tc_sp24", "tc_pipe_sp24", "tc_pipe_dense"]
 
 
 def _set(plan, algo):
-    for suffix, onehot in (("_sp24", "sparse24"), ("_dense", "dense"), ("_sel", "select")):
+    for suffix, onehot in (("_sp24", "sparse24"), ("_dense", "dense")):
         if algo.endswith(suffix):
             plan.set_algo(algo[: -len(suffix)])
             plan.set_onehot(onehot)
@@ -338,7 +336,7 @@ def test_parity_one_cta_streamed_lut_kernel():
         "    ref = oracle.amm(p, w['A'], relu=w['relu'], dtype=dt, nthreads=8)['y']\n"
         "    A = torch.from_numpy(w['A'].view(np.int16) if dt == 'bf16' else w['A']).cuda()\n"
         "    A = A.view(torch.bfloat16) if dt == 'bf16' else A\n"
-        "    for oh in ('dense', 'sparse24', 'select'):\n"
+        "    for oh in ('dense', 'sparse24'):\n"
         "        pl = Plan(p); pl.set_onehot(oh)\n"
         "        y = pl.amm(A, relu=w['relu']).cpu().numpy()\n"
         "        assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), (seed, oh)\n"

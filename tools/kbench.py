@@ -92,7 +92,7 @@ def main():
     for algo in args.algos.split(","):
         try:
             base, onehot = algo, "auto"
-            for suffix, oh in (("_sp24", "sparse24"), ("_dense", "dense"), ("_sel", "select")):
+            for suffix, oh in (("_sp24", "sparse24"), ("_dense", "dense")):
                 if algo.endswith(suffix):
                     base, onehot = algo[: -len(suffix)], oh
             plan.set_algo(base)

@@ -37,7 +37,7 @@ KE = 512
 buf = np.zeros(16 * 4 * KE, np.uint64)
 assert lib.itlumm_dbg_trace_copy(plan._h, buf.ctypes.data_as(ctypes.c_void_p), buf.size) == 0
 W = 64
-t = buf[:2 * 16 * W].reshape(2, 16, W).astype(np.int64)      # [CTA][slot][stage - 96]
+t = buf[:2 * 24 * W].reshape(2, 24, W)[:, :16].astype(np.int64)   # [CTA][slot][stage - 96]
 t0 = t[0][t[0] > 0].min()
 S = lambda c, slot: np.where(t[c, slot] > 0, t[c, slot] - t0, -1)  # noqa: E731
 mw, mi, l0, l1 = S(0, 0), S(0, 1), S(0, 2), S(1, 3)
