@@ -95,6 +95,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def acc_kernel_name(C, M):
+    """Which accumulate kernel AUTO runs (the rule of tc_layout_host, csrc/tc.cuh): the LUT stays
+    resident in shared memory (1-CTA k_tc) unless that would force slices narrower than 256 columns;
+    a streamed LUT runs on CTA pairs (k_tcp)."""
+    kb = (16 * C + 127) // 128
+    ns_max = (128 * 1024 // (kb * 128)) // 32 * 32
+    streamed = ns_max < 32 or (ns_max < 256 and M > ns_max)
+    return ("k_tcp (a3' one-hot x LUT, tcgen05 CTA pairs, streamed LUT, + a4)" if streamed
+            else "k_tc (a3' one-hot x LUT on tcgen05, resident LUT, + a4)")
+
+
 def i8_peaks():
     """Two dense int8 peaks for the one-hot x LUT contraction: the measured bf16 GEMM burst
     (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio 2 (4.5 / 2.25 PFLOP/s dense), and the
@@ -304,7 +315,7 @@ def run_ours(args):
              "achieved_GBps": b_enc / (t_enc * 1e-3) / 1e9,
              "note": ("split-packed rows: 4C values per row, contiguous" if packed else
                       "reads whole rows: the 4C split columns touch ~every DRAM line of a row")},
-            {"kernel": "k_tc (a3' one-hot x LUT on tcgen05 + a4)", "ms": t_acc, "alg_bytes": b_acc,
+            {"kernel": acc_kernel_name(cfg["C"], cfg["M"]), "ms": t_acc, "alg_bytes": b_acc,
              "achieved_GBps": b_acc / (t_acc * 1e-3) / 1e9},
         ]
         del g_enc, g_acc

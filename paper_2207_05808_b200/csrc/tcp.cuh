@@ -41,6 +41,7 @@ constexpr int kTcpDense = 0, kTcpSparse = 1;   // k_tcp MODE
 // SMSP 0 hosts the MMA issuer and the loader (and the two quadrant-0 epilogue warps), no producer:
 // producer warps sharing the issuer's SMSP ran ~3000 cycles behind the other producers every stage
 // (tcp_trace, profiles/r02): the issuer's tcgen05 ops take ~40 cycles of its SMSP each.
+constexpr int kTcpSsMax = 3;           // K-blocks per ring slot at most
 constexpr int kTcpProdWarps = 8;
 constexpr int kTcpEpiWarps = 8;
 constexpr int kTcpMmaWarp = 0;
@@ -198,7 +199,8 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   extern __shared__ __align__(1024) uint8_t smem_tcp[];
   uint8_t* smem = smem_tcp + ((1024u - (smem_u32(smem_tcp) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G, ST = g.ST, CS = g.CS, SS = g.SS;
-  const int KBS = KB / SS;                 // ring slots per item
+  const int KBS = (KB + SS - 1) / SS;      // ring slots per item (the last may hold fewer K-blocks)
+  auto nsub = [&](int kb) { return KB - kb * SS < SS ? KB - kb * SS : SS; };   // K-blocks in slot kb
   const TcpSmem L = tcp_smem_layout(MODE, NS, ST, CS, (int)g.ldc, g.trace != nullptr, SS);
   uint8_t* ring = smem + L.ring;
   uint8_t* codes_s = smem + L.codes;
@@ -320,8 +322,9 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           if (g.dbg & 4) {
             if (rank == 0) mbar_arrive(full_bar + st);
           } else {
-            if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * bhalf * SS);
-            for (int j = 0; j < SS; ++j)
+            const int ns = nsub(kb);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar + st, 2 * bhalf * ns);
+            for (int j = 0; j < ns; ++j)
               tma_load_2d_pair(ring + (size_t)(st * SS + j) * L.stage + L.a_bytes + L.e_bytes, &qt_map, 0,
                                y0 + (kb * SS + j) * NS, full_leader + 8u * st);
           }
@@ -378,8 +381,10 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
       // stage's slot to free up (one MMA pass later), which cost more than the fence it saved
       for (int kb = 0; kb < KBS; ++kb) {
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          if (jj >= SS) break;
+        const int ns = nsub(kb);
+#pragma unroll
+        for (int jj = 0; jj < kTcpSsMax; ++jj) {
+          if (jj >= ns) break;
           const int kbi = kb * SS + jj;
           if ((kbi & 3) == 0) {                          // 4 K-blocks of codes
             if (cdir) {
@@ -475,9 +480,10 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         }
       };
       auto issue_slot = [&](int slot, int kb, uint32_t d) {   // the SS K-blocks of one ring slot
+        const int ns = nsub(kb);
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (j < SS) issue(slot * SS + j, kb * SS + j, d);
+        for (int j = 0; j < kTcpSsMax; ++j)
+          if (j < ns) issue(slot * SS + j, kb * SS + j, d);
       };
       for (int64_t k = 0; item(k, tile, sl); ++k) {
         mbar_wait(acce_bar + acc, aph ^ 1);   // both CTAs' epilogues drained this accumulator
@@ -623,14 +629,16 @@ inline void tcp_finish(TcpPlan& t, int C, int row_bytes) {
   const int ldc_max = 16 * ((C + 31) / 32);
   static const int st_env = getenv("ITLUMM_TCP_STAGES") ? atoi(getenv("ITLUMM_TCP_STAGES")) : 0;   // developer
   static const int ss_env = getenv("ITLUMM_TCP_SS") ? atoi(getenv("ITLUMM_TCP_SS")) : 2;   // developer
-  t.SS = (t.mode == kTcpDense && ss_env == 2 && t.KB % 2 == 0) ? 2 : 1;
+  t.SS = ss_env < 1 ? 1 : ss_env > kTcpSsMax ? kTcpSsMax : ss_env;
+  if (t.SS > t.KB) t.SS = t.KB;
   static const int cd_env = getenv("ITLUMM_TCP_CDIRECT") ? atoi(getenv("ITLUMM_TCP_CDIRECT")) : 1;   // developer
   t.CS = cd_env ? 0 : 2;   // 0: codes straight from global memory, the space goes to the ring
   int ST = 12;
   while (ST > 2 && tcp_smem_layout(t.mode, t.NS, ST, t.CS, ldc_max, false, t.SS).total > kSmemMax) --ST;
+  while (t.SS > 1 && tcp_smem_layout(t.mode, t.NS, 2, t.CS, ldc_max, false, t.SS).total > kSmemMax) --t.SS;   // two slots at least
   if (st_env >= 2 && st_env < ST) ST = st_env;
   const int meta_cols = t.mode == kTcpSparse ? 4 : 0;
-  if (meta_cols && 2 * t.NS + meta_cols * ST > 512) ST = (512 - 2 * t.NS) / meta_cols;
+  if (meta_cols && 2 * t.NS + meta_cols * ST * t.SS > 512) ST = (512 - 2 * t.NS) / (meta_cols * t.SS);
   if (ST < 2) { t.why = "shared memory / TMEM budget"; return; }
   t.ST = ST;
   auto enc = tensor_map_encoder();
