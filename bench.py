@@ -169,7 +169,7 @@ class ClockSampler:
         with open(self.out.name) as f:
             lines = [l.strip() for l in f if l.strip()]
         os.unlink(self.out.name)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in lines:
             parts = [p.strip() for p in l.split(",")]
@@ -180,13 +180,21 @@ class ClockSampler:
                 mx = float(parts[3])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[4]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:   # the board limit is ~1000 W: sw_power_cap with the power at it means power-bound
+            out["power_w_median"] = float(np.median(pw))
+            out["power_w_max"] = float(max(pw))
+        return out
 
 
 # --------------------------------------------------------------------------------- ours
