@@ -14,17 +14,25 @@
 //   * a CTA pair stages HALF of every LUT K-block per SM (each LUT byte fetched from L2 feeds 256
 //     rows), which halves the L2 -> shared-memory stream that the streamed LUT needs.
 //
-// Per pair item = (256 rows, one NS-column slice), CTA r of the pair owns rows [128r, 128r+128):
-//   warps 0-3   producers: one row each; per 8-codebook K-block the row's 2:4-compressed one-hot
-//               (8 B per codebook, K-major SWIZZLE_64B) and its metadata (16 B, for tcgen05.cp) go to
-//               ring stage st; fence.proxy.async; per-warp arrive on the LEADER's full[st].
-//   warp 4      MMA issuer (leader CTA only): tcgen05.cp.cta_group::2 of both CTAs' metadata to TMEM,
-//               two tcgen05.mma.sp.cta_group::2.kind::i8 (M=256, N=NS, K=64), commits multicast to
-//               both CTAs (stage free; accumulator ready).  Dense variant (SP=false): 4 K=32 MMAs.
-//   warps 5-12  epilogue (each CTA its own 128 rows): tcgen05.ld -> fmaf (+ReLU) -> 128B-swizzled
-//               staging -> TMA tensor store of 32x32 boxes; per-warp arrive on the leader's acce.
-//   warp 13     loader: the CTA's 128-row codes tile (bulk copy) and its half of each LUT K-block
-//               (TMA tensor load .cta_group::2: the bytes complete on the LEADER's full[st]).
+// Per pair item = (256 rows, one NS-column slice), CTA r of the pair owns rows [128r, 128r+128).
+// The ring moves in SLOTS of SS K-blocks (8 codebooks each; SS = 2 by default): one barrier round
+// trip, one producer proxy fence + arrive and one MMA commit per slot.  The bare handshakes cost as
+// much per slot as per K-block, so two K-blocks per slot halved them (cfg5 accumulate 3.68 -> 2.93
+// ms on one box).  Roles (warp -> role: tcp_role):
+//   producers (8 warps, SMSPs 1-3)  two threads per row; per K-block of the slot the row's one-hot
+//               (dense: 16 B per codebook, K-major SWIZZLE_128B; 2:4-sparse: 8 B per codebook,
+//               SWIZZLE_64B, + 16 B of metadata for tcgen05.cp); fence.proxy.async; one arrive per
+//               warp and slot on the LEADER's full[st].
+//   MMA issuer (warp 0, leader CTA only)  per K-block 4 tcgen05.mma.cta_group::2.kind::i8 (M=256,
+//               N=NS, K=32) or, 2:4-sparse, one tcgen05.cp.cta_group::2 of both CTAs' metadata and 2
+//               tcgen05.mma.sp (K=64); commits multicast to both CTAs (slot free; accumulator ready).
+//   epilogue (8 warps, two per TMEM lane quadrant)  each CTA its own 128 rows: tcgen05.ld -> fmaf
+//               (+ReLU) -> 128B-swizzled staging -> TMA tensor store of 32x32 boxes; per-warp
+//               arrive on the leader's acce.
+//   LUT loader (warp 4)  its half of each LUT K-block (TMA tensor load .cta_group::2: the bytes
+//               complete on the LEADER's full[st]).
+//   codes loader (warp 16)  the CTA's 128-row codes tile per item (bulk copy), up to CS items ahead;
+//               with CS = 0 (developer option) the producers load their codes from global memory.
 // Results are bit-identical to every other schedule (exact integer MMA, the same single fmaf).
 #pragma once
 #include "tc.cuh"
