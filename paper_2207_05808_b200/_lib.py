@@ -8,6 +8,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libitlumm.so")
+# developer A/B runs only (tools/): another build of the same library; never set by the tests or bench
+LIB_PATH = os.environ.get("ITLUMM_DEV_LIB", LIB_PATH)
 
 OK, EINVAL, ESHAPE, EUNSUPPORTED, ECUDA, ENOMEM = range(6)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA", 5: "ENOMEM"}

@@ -254,7 +254,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
   s.sc = o;   o += (size_t)NS * 4;
   s.ot = o;   o += (size_t)NS * 4;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;  o += (size_t)(2 * ST + 4 + 2 * CS + 1) * 8;
+  s.bar = o;  o += (size_t)(2 * ST + 4 + 2 * CS + (stream_b ? 1 : KB)) * 8;
   s.tmem = o; o += 16;
   s.total = o + 1024;                           // slack for 1024-byte alignment of the base
   return s;
@@ -284,7 +284,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   uint64_t* acce_bar = accf_bar + 2;
   uint64_t* codes_bar = acce_bar + 2;
   uint64_t* codes_empty = codes_bar + CS;            // producers done with a codes stage
-  uint64_t* b_bar = codes_empty + CS;                // resident LUT slice landed
+  uint64_t* b_bar = codes_empty + CS;                // resident LUT slice: K-block kb landed (b_bar[kb])
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
 
   const int slice = cta % G;
@@ -347,13 +347,16 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   // thresholds, columns, scales by the threads; only the MMA warp waits for the slice.
   {
     if (threadIdx.x == 0 && !SB) {
-      mbar_init(b_bar, 1);
+      // one barrier per K-block (NS x 128 B <= 32 KB): the first item's MMAs start on K-block 0
+      // while the rest of the slice is still landing
+      for (int kb = 0; kb < KB; ++kb) mbar_init(b_bar + kb, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       const uint8_t* src = g.qt + (size_t)slice * KB * NS * kKBlock;
-      const uint32_t total = (uint32_t)KB * NS * kKBlock;
-      mbar_arrive_expect_tx(b_bar, total);
-      for (uint32_t o = 0; o < total; o += 32768u)
-        bulk_g2s(b_s + o, src + o, (total - o) < 32768u ? (total - o) : 32768u, b_bar);
+      const uint32_t blk = (uint32_t)NS * kKBlock;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_arrive_expect_tx(b_bar + kb, blk);
+        bulk_g2s(b_s + (size_t)kb * blk, src + (size_t)kb * blk, blk, b_bar + kb);
+      }
     }
     if (FUSED) {
       for (int i = threadIdx.x; i < C * 16; i += blockDim.x) {
@@ -553,7 +556,6 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       // lane issues each tcgen05 op (a lone lane == 0 thread wrapped every op in an elect loop and
       // moved every descriptor through R2UR: ~190 ns per stage in the k_tcp timeline, profiles/r02)
       const uint32_t idesc = idesc_i8(NS);
-      if (!SB) mbar_wait(b_bar, 0);                  // resident LUT slice in shared memory
       const uint32_t a0 = smem_u32(a_s);
       const uint64_t a_desc0 = SP ? umma_desc_sw64(a0) : umma_desc_sw128(a0);
       const uint64_t m_desc0 = umma_desc_rows16(a0 + kSpA);
@@ -571,6 +573,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * NS);
         for (int kb = 0; kb < KB; ++kb) {
+          if (!SB && k == 0) mbar_wait(b_bar + kb, 0);   // the resident LUT slice's K-block kb
           mbar_wait(full_bar + stage, phase);
           const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((SB ? stage : kb) * b_step);
