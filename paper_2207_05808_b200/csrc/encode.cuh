@@ -16,8 +16,8 @@
 
 namespace itlumm {
 
-constexpr int kEncConsumerWarps = 8;
-constexpr int kEncThreads = 32 * (1 + kEncConsumerWarps);   // warp 0: bulk-copy producer
+constexpr int kEncConsumerWarps = 16;                         // default consumer warps
+constexpr int kEncMaxConsumerWarps = 24;
 
 struct EncArgs {
   const void* A;
@@ -255,7 +255,7 @@ __device__ __forceinline__ void enc_cta(const DevPlan& p, const EncArgs& g, uint
 }
 
 template <typename T, bool WIDE>
-__global__ void __launch_bounds__(kEncThreads, 1) k_encode_rows(DevPlan p, EncArgs g) {
+__global__ void __launch_bounds__(32 * (1 + kEncMaxConsumerWarps), 1) k_encode_rows(DevPlan p, EncArgs g) {
   extern __shared__ __align__(16) uint8_t smem_enc[];
   enc_cta<T, WIDE>(p, g, smem_enc, blockIdx.x, gridDim.x);
 }

@@ -447,15 +447,18 @@ static itlumm_status check_dev(itlumm_plan P, const void* ptr, const char* what)
 // Rows per stage R and ring depth S of the streaming encoder for rows of rb bytes, or false if
 // the rows cannot be bulk-copied.
 static bool enc_tiling(itlumm_plan P, int64_t rb, int consumer_warps, int* Rout, int* Sout,
-                       int inflight_override_kb = 0, int max_stages = 8) {
+                       int inflight_override_kb = 0, int max_stages = 8, int64_t N = 0) {
   // ~24 KB stages and ~100 KB in flight per SM: the measured optimum of a cfg2 sweep (more
   // bytes in flight lowered DRAM efficiency: 6.1 TB/s at 4 x 25 KB vs 5.5 TB/s at 6 x 31 KB,
   // profiles/r01/encode_stage_sweep.txt).  Developer overrides (not ABI):
   // ITLUMM_ENC_STAGE_KB, ITLUMM_ENC_INFLIGHT_KB.
   // 48 KB stages where the consumers are compute-heavy (C >= 128: the per-tile handshake is amortised
-  // over twice the rows; D=592 C=256 encode 294 -> 263 us)
+  // over twice the rows; D=592 C=256 encode 294 -> 263 us) and, with 16 consumer warps, wherever the
+  // call has a full wave of 48 KB tiles (cfg2 packed encode 12.3 -> 9.9 us, row-major 32.1 -> 30.8 us,
+  // cfg3 C=128 packed 34.7 -> 24.9 us, measured with 16 warps; tools/gpu_encwarps.sh)
   static const int stage_kb_env = getenv("ITLUMM_ENC_STAGE_KB") ? atoi(getenv("ITLUMM_ENC_STAGE_KB")) : 0;
-  const int stage_kb = stage_kb_env > 0 ? stage_kb_env : (P->C >= 128 ? 48 : 24);
+  const bool big = P->C >= 128 || N * rb >= (int64_t)P->num_sms * 48 * 1024;
+  const int stage_kb = stage_kb_env > 0 ? stage_kb_env : (big ? 48 : 24);
   static const int inflight_kb = getenv("ITLUMM_ENC_INFLIGHT_KB") ? atoi(getenv("ITLUMM_ENC_INFLIGHT_KB")) : 100;
   if (rb > 64 * 1024) return false;
   const int ngrp = (P->C + 31) / 32;
@@ -485,7 +488,12 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
   // the columns per thread when they touch few of them (cfg4 C=16 layer 1: 64 of 3072 columns).
   const bool sparse_cols = P->seg_frac[dtype == ITLUMM_BF16 ? 1 : 0] < 0.6;
   int R = 0, S = 0;
-  if (aligned && !sparse_cols && enc_tiling(P, rb, kEncConsumerWarps, &R, &S)) {
+  // 16 consumer warps: with 8 the encoder was latency-bound (ncu: 14% warps active, 32% issue) on
+  // split-packed rows, whose tree walks per byte are 6x those of row-major cfg2 rows.  Developer
+  // override: ITLUMM_ENC_WARPS.
+  static const int enc_warps_env = getenv("ITLUMM_ENC_WARPS") ? atoi(getenv("ITLUMM_ENC_WARPS")) : 0;
+  const int enc_warps = enc_warps_env > 0 ? std::min(enc_warps_env, kEncMaxConsumerWarps) : kEncConsumerWarps;
+  if (aligned && !sparse_cols && enc_tiling(P, rb, enc_warps, &R, &S, 0, 8, N)) {
     {
       EncArgs g{};
       g.A = A; g.lda = lda; g.N = N; g.codes = codes; g.ldc = ldc;
@@ -514,7 +522,7 @@ static itlumm_status launch_encode(itlumm_plan P, const void* A, itlumm_dtype dt
       g.pdl_wait = (pdl_dep && (dep_env == 2 || (dep_env == 1 && ntiles <= P->num_sms))) ? 1 : 0;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(kEncThreads);
+      cfg.blockDim = dim3(32 * (1 + enc_warps));
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];

@@ -6,7 +6,7 @@ shift
 WL=${@:-cfg2 cfg2p cfg1}
 mkdir -p gpurun_out
 L=gpurun_out/ablib_$TAG.log
-timeout 900 python -m pytest tests/test_parity_gpu.py -q -m gpu -p no:cacheprovider -k "small or cfg1 or cfg2 or edge or mlp" > gpurun_out/pytest_$TAG.log 2>&1; echo rc=$? >> gpurun_out/pytest_$TAG.log
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -m gpu -p no:cacheprovider -k "${PYK:-small or cfg1 or cfg2 or edge or mlp}" > gpurun_out/pytest_$TAG.log 2>&1; echo rc=$? >> gpurun_out/pytest_$TAG.log
 for rep in 1 2; do
   for lib in ref new; do
     for w in $WL; do
@@ -14,7 +14,7 @@ for rep in 1 2; do
       if [ "${w: -1}" = "p" ]; then P="--packed"; W=${w%p}; fi
       echo "lib=$lib rep=$rep $w" >> $L
       if [ $lib = ref ]; then export ITLUMM_DEV_LIB=$PWD/paper_2207_05808_b200/lib/libitlumm_ref.so; else unset ITLUMM_DEV_LIB; fi
-      timeout 300 python tools/kbench.py --workload $W $P --algos tc_pipe --only acc,fused --iters 100 >> $L 2>&1
+      timeout 300 python tools/kbench.py --workload $W $P --algos tc_pipe --only encode,acc,fused --iters ${ITERS:-100} >> $L 2>&1
     done
   done
 done
