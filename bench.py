@@ -191,9 +191,8 @@ class ClockSampler:
             return None
         out = {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": mx,
                "reasons": sorted(reasons), "samples": len(sm)}
-        if pw:   # the board limit is ~1000 W: sw_power_cap with the power at it means power-bound
-            out["power_w_median"] = float(np.median(pw))
-            out["power_w_max"] = float(max(pw))
+        if pw:   # nvidia-smi power.draw is a ~1 s average: it lags a short timed region (only the max
+            out["power_w_max_1s_avg"] = float(max(pw))   # is reported; tools/clock_probe.py measures sustained power)
         return out
 
 
