@@ -21,6 +21,11 @@ def _np_ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+def _ld(t):
+    """Row stride in elements; a 1-row tensor's stride(0) is arbitrary in torch, so its row length."""
+    return t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[1])
+
+
 def _stream(stream, device):
     """A raw cudaStream_t: `stream` (a torch.cuda.Stream or an int handle), else the current stream of
     the plan's device."""
@@ -135,8 +140,8 @@ class Plan:
             codes = torch.empty((N, (self.C + 1) // 2), dtype=torch.uint8, device=A.device)
         _check(codes, "codes", (torch.uint8,), N, (self.C + 1) // 2, self.device)
         _lib.check(self._lib.itlumm_encode(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
-                                           A.stride(0), N, ctypes.c_void_p(codes.data_ptr()),
-                                           codes.stride(0), _stream(stream, self.device)))
+                                           _ld(A), N, ctypes.c_void_p(codes.data_ptr()),
+                                           _ld(codes), _stream(stream, self.device)))
         return codes
 
     def lut_accumulate(self, codes, out=None, acc=None, relu=False, want_out=True, stream=None):
@@ -150,11 +155,11 @@ class Plan:
         if acc is not None:
             _check(acc, "acc", (torch.int32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_lut_accumulate(
-            self._h, ctypes.c_void_p(codes.data_ptr()), codes.stride(0), N,
+            self._h, ctypes.c_void_p(codes.data_ptr()), _ld(codes), N,
             ctypes.c_void_p(acc.data_ptr()) if acc is not None else None,
-            acc.stride(0) if acc is not None else self.M,
+            _ld(acc) if acc is not None else self.M,
             ctypes.c_void_p(out.data_ptr()) if out is not None else None,
-            out.stride(0) if out is not None else self.M,
+            _ld(out) if out is not None else self.M,
             _lib.EPI_RELU if relu else _lib.EPI_NONE, _stream(stream, self.device)))
         return out, acc
 
@@ -167,8 +172,8 @@ class Plan:
             out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
         _check(out, "out", (torch.float32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_amm(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
-                                        A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
-                                        out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
+                                        _ld(A), N, ctypes.c_void_p(out.data_ptr()),
+                                        _ld(out), _lib.EPI_RELU if relu else _lib.EPI_NONE,
                                         _stream(stream, self.device)))
         return out
 
@@ -183,8 +188,8 @@ class Plan:
             out = torch.empty((N, self.M), dtype=torch.float32, pin_memory=A.is_pinned())
         _check(out, "out", (torch.float32,), N, self.M)
         _lib.check(self._lib.itlumm_amm_host(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
-                                             A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
-                                             out.stride(0), _lib.EPI_RELU if relu else _lib.EPI_NONE,
+                                             _ld(A), N, ctypes.c_void_p(out.data_ptr()),
+                                             _ld(out), _lib.EPI_RELU if relu else _lib.EPI_NONE,
                                              _stream(stream, self.device)))
         return out
 
@@ -222,8 +227,8 @@ class Mlp:
             out = torch.empty((N, self.M), dtype=torch.float32, device=A.device)
         _check(out, "out", (torch.float32,), N, self.M, self.device)
         _lib.check(self._lib.itlumm_mlp_forward(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
-                                                A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
-                                                out.stride(0), _stream(stream, self.device)))
+                                                _ld(A), N, ctypes.c_void_p(out.data_ptr()),
+                                                _ld(out), _stream(stream, self.device)))
         return out
 
     def forward_host(self, A, out=None, stream=None):
@@ -236,8 +241,8 @@ class Mlp:
             out = torch.empty((N, self.M), dtype=torch.float32, pin_memory=A.is_pinned())
         _check(out, "out", (torch.float32,), N, self.M)
         _lib.check(self._lib.itlumm_mlp_forward_host(self._h, ctypes.c_void_p(A.data_ptr()), _dtype_code(A),
-                                                     A.stride(0), N, ctypes.c_void_p(out.data_ptr()),
-                                                     out.stride(0), _stream(stream, self.device)))
+                                                     _ld(A), N, ctypes.c_void_p(out.data_ptr()),
+                                                     _ld(out), _stream(stream, self.device)))
         return out
 
     def close(self):

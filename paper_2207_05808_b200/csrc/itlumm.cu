@@ -613,6 +613,7 @@ static itlumm_status launch_lut(itlumm_plan P, bool fused, const void* A, itlumm
     TcArgs a{};
     a.A = A; a.lda = lda; a.codes = codes; a.ldc = ldc; a.N = N; a.acc = acc; a.ldacc = ldacc;
     a.out = out; a.ldo = ldo; a.relu = epi == ITLUMM_EPI_RELU;
+    a.packed = P->packed ? 1 : 0;
     itlumm_status st = fused ? tc_launch(t, P->dp, true, dtype == ITLUMM_BF16, a, s) : launch_tc_acc(P, a, s, false);
     if (st == ITLUMM_OK) {
       g_launches = 1;

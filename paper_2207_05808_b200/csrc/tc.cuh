@@ -65,6 +65,7 @@ struct TcPlan {
 struct TcArgs {
   const void* A; int64_t lda; const uint8_t* codes; int64_t ldc; int64_t N;
   int32_t* acc; int64_t ldacc; float* out; int64_t ldo; int relu;
+  int packed = 0;  // fused: split-packed rows (gather column of (c, t) is 4c + t) with 16-B aligned rows
 };
 
 struct TcKArgs {
@@ -74,6 +75,9 @@ struct TcKArgs {
   int32_t* acc; int64_t ldacc;
   float* out; int64_t ldo;
   int relu;
+  int packed;      // fused producers: split-packed rows, one vector load per codebook
+  int a_tma;       // fused, resident LUT, f32 split-packed rows: the loader warp stages each K-block's
+                   // 128 rows x 32 floats by TMA (a_map, SWIZZLE_128B) into the one-hot stage itself
   const uint8_t* qt;
   int KB, NS, G, tmem_cols;
   int CS;          // codes ring stages; > 0 selects the bulk-copy (TMA) codes path
@@ -106,6 +110,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int x, int y, uint64_t pol) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol) : "memory");
+}
+// TMA tensor load of one box at (x, y) into shared memory, completing on `mbar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(mbar)) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -254,7 +263,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
   s.sc = o;   o += (size_t)NS * 4;
   s.ot = o;   o += (size_t)NS * 4;
   o = (o + 7) & ~(size_t)7;
-  s.bar = o;  o += (size_t)(2 * ST + 4 + 2 * CS + (stream_b ? 1 : KB)) * 8;
+  s.bar = o;  o += (size_t)(3 * ST + 4 + 2 * CS + (stream_b ? 1 : KB)) * 8;   // + ST a_full (fused TMA rows)
   s.tmem = o; o += 16;
   s.total = o + 1024;                           // slack for 1024-byte alignment of the base
   return s;
@@ -263,7 +272,7 @@ __host__ __device__ inline TcSmem tc_smem_layout(int C, int KB, int NS, int CS =
 // One persistent CTA of the tensor-core kernel: CTA `cta` of `ncta` (slice = cta % G).
 template <bool FUSED, typename T, bool SB, bool SP = false>
 __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const CUtensorMap* out_map,
-                                       uint8_t* smem_raw, int cta, int ncta) {
+                                       const CUtensorMap* a_map, uint8_t* smem_raw, int cta, int ncta) {
   // align in the shared window without leaving the shared address space (keeps LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int C = p.C, KB = g.KB, NS = g.NS, G = g.G;
@@ -285,6 +294,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
   uint64_t* codes_bar = acce_bar + 2;
   uint64_t* codes_empty = codes_bar + CS;            // producers done with a codes stage
   uint64_t* b_bar = codes_empty + CS;                // resident LUT slice: K-block kb landed (b_bar[kb])
+  uint64_t* afull_bar = b_bar + (SB ? 1 : KB);        // fused TMA rows: the stage's A rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
 
   const int slice = cta % G;
@@ -371,7 +381,7 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
       ot_s[i] = m < p.Mp ? __ldg(p.offtot + m) : 0.f;
     }
     if (threadIdx.x == 0) {
-      for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, kTcProducers + (SB ? 1 : 0)); mbar_init(empty_bar + s, 1); }
+      for (int s = 0; s < ST; ++s) { mbar_init(full_bar + s, kTcProducers + (SB ? 1 : 0)); mbar_init(empty_bar + s, 1); mbar_init(afull_bar + s, 1); }
       for (int a = 0; a < 2; ++a) { mbar_init(accf_bar + a, 1); mbar_init(acce_bar + a, kTcEpiThreads); }
       for (int s = 0; s < CS; ++s) { mbar_init(codes_bar + s, 1); mbar_init(codes_empty + s, kTcProducers); }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -395,7 +405,24 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     // ============================================================== codes loader (one lane)
     // Codes tiles (128 rows x ldc bytes, contiguous) through a CS-deep bulk-copy ring (when the
     // codes rows can be bulk-copied), and with a streamed LUT (SB) the item's LUT K-blocks.
-    if (lane == 0 && ((!FUSED && CS > 0) || SB)) {
+    if (lane == 0 && FUSED && !SB && g.a_tma) {
+      // fused, split-packed f32 rows: K-block kb of a tile is the box (x = 32 kb, y = 128 tile) of
+      // 128 rows x 128 B, loaded into the one-hot stage the producers then overwrite in place
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a_map)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t k = 0; item(k, tile, sl); ++k) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(empty_bar + stage, phase ^ 1);    // MMA finished reading this stage
+          mbar_arrive_expect_tx(afull_bar + stage, (uint32_t)(kTcRows * kKBlock));
+          tma_load_2d(a_s + (size_t)stage * kAStage, a_map, 32 * kb, (int)(tile * kTcRows), afull_bar + stage);
+          stamp(3);
+          if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else if (lane == 0 && ((!FUSED && CS > 0) || SB)) {
       int cs = 0, stage = 0;
       uint32_t cph = 0, phase = 0;
       int64_t tile;
@@ -465,6 +492,43 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
         mbar_arrive(codes_empty + cs);                 // this producer is done with stage cs
         if (++cs == CS) { cs = 0; cph ^= 1; }
       }
+    } else if (FUSED && !SB && !SP && g.a_tma) {
+      // Row r's 8 codebooks x 4 split values landed by TMA as row r of the stage (chunk j of the
+      // 128 B at 16 (j ^ (r & 7)), SWIZZLE_128B: conflict-free reads); the thread walks the 8 trees
+      // and overwrites exactly those 128 B with its one-hot row (the same swizzled chunks).
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t tile;
+      int sl;
+      for (int64_t kk = 0; item(kk, tile, sl); ++kk) {
+        const bool valid = tile * kTcRows + r < g.N;
+        for (int kb = 0; kb < KB; ++kb) {
+          uint8_t* st = a_s + (size_t)stage * kAStage;
+          mbar_wait(afull_bar + stage, phase);
+          float4 q[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) q[j] = *reinterpret_cast<const float4*>(st + sw128_off(r, j));
+          uint32_t code[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = kb * 8 + j;
+            code[j] = 16;
+            if (valid && c < C) {
+              const float* th = thr_s + c * 16;
+              const float vv[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+              int node = 0;
+#pragma unroll
+              for (int t = 0; t < kLevels; ++t) node = 2 * node + (vv[t] > th[(1 << t) - 1 + node] ? 1 : 0);
+              code[j] = (uint32_t)node;
+            }
+          }
+          put_onehot<false>(st, r, code);
+          fence_proxy_async_smem();
+          mbar_arrive(full_bar + stage);
+          if (r == 0) stamp(0);
+          if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+      }
     } else {
     const bool codes_u32 = !FUSED && ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(g.codes) & 3) == 0);
     int stage = 0;
@@ -474,7 +538,25 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
     auto load = [&](int64_t tile, int kb, float (&v)[8][4], uint32_t& cw) {
       const int64_t row = tile * kTcRows + r;
       if (row >= g.N) return;
-      if (FUSED) {
+      if (FUSED && g.packed) {
+        // split-packed row: codebook c's four split values are a[4c..4c+3], one 16-byte (f32) or
+        // 8-byte (bf16) load each; the 8 loads of a K-block cover 128 (64) contiguous bytes
+        const T* a = reinterpret_cast<const T*>(g.A) + row * g.lda;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = kb * 8 + j;
+          if (c < C) {
+            if (sizeof(T) == 4) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(a + 4 * c));
+              v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
+            } else {
+              const uint2 q = __ldg(reinterpret_cast<const uint2*>(a + 4 * c));
+              v[j][0] = __uint_as_float(q.x << 16); v[j][1] = __uint_as_float(q.x & 0xFFFF0000u);
+              v[j][2] = __uint_as_float(q.y << 16); v[j][3] = __uint_as_float(q.y & 0xFFFF0000u);
+            }
+          }
+        }
+      } else if (FUSED) {
         const T* a = reinterpret_cast<const T*>(g.A) + row * g.lda;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -789,9 +871,10 @@ __device__ __forceinline__ void tc_cta(const DevPlan& p, const TcKArgs& g, const
 }
 
 template <bool FUSED, typename T, bool SB, bool SP = false>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc(DevPlan p, TcKArgs g, const __grid_constant__ CUtensorMap out_map,
+                                                      const __grid_constant__ CUtensorMap a_map) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  tc_cta<FUSED, T, SB, SP>(p, g, &out_map, smem_raw, blockIdx.x, gridDim.x);
+  tc_cta<FUSED, T, SB, SP>(p, g, &out_map, &a_map, smem_raw, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -927,6 +1010,8 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   TcKArgs k{};
   k.A = a.A; k.lda = a.lda; k.codes = a.codes; k.ldc = a.ldc; k.N = a.N;
   k.acc = a.acc; k.ldacc = a.ldacc; k.out = a.out; k.ldo = a.ldo; k.relu = a.relu;
+  k.packed = fused && a.packed && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 &&
+             (a.lda * (bf16 ? 2 : 4)) % 16 == 0 ? 1 : 0;
   k.qt = t.qt; k.KB = t.KB; k.NS = t.NS; k.G = t.G; k.tmem_cols = t.tmem_cols;
   k.pdl = pdl ? 1 : 0;
   k.stream_b = t.stream_b ? 1 : 0;
@@ -939,6 +1024,22 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   alignas(64) CUtensorMap out_map;
   memset(&out_map, 0, sizeof out_map);
   k.tma_store = (!a.acc && make_out_map(&out_map, a.out, a.N, t.M, a.ldo)) ? 1 : 0;
+  // fused over split-packed f32 rows with a resident LUT: rows staged by TMA (developer override,
+  // not ABI: ITLUMM_TC_ATMA=0 keeps the per-thread vector loads)
+  static const int atma_env = getenv("ITLUMM_TC_ATMA") ? atoi(getenv("ITLUMM_TC_ATMA")) : 1;
+  alignas(64) CUtensorMap a_map;
+  memset(&a_map, 0, sizeof a_map);
+  k.a_tma = 0;
+  if (atma_env && k.packed && !bf16 && !t.stream_b && !t.sp && t.C >= 8 && a.N <= INT32_MAX) {
+    auto enc = tensor_map_encoder();
+    const cuuint64_t dims[2] = {(cuuint64_t)4 * t.C, (cuuint64_t)a.N};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.lda * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)kTcRows};
+    const cuuint32_t estr[2] = {1, 1};
+    k.a_tma = enc && enc(&a_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(a.A), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS ? 1 : 0;
+  }
   size_t smem = t.smem;
   if (fused && t.stream_b) {
     // fused over a streamed LUT: the threshold/column tables sit next to the LUT ring
@@ -970,22 +1071,22 @@ inline itlumm_status tc_launch(const TcPlan& t, const DevPlan& dp, bool fused, b
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e;
   if (t.sp) {
-    if (fused && t.stream_b) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true, true>, dp, k, out_map)
-                                      : cudaLaunchKernelEx(&cfg, k_tc<true, float, true, true>, dp, k, out_map);
-    else if (fused) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false, true>, dp, k, out_map)
-                             : cudaLaunchKernelEx(&cfg, k_tc<true, float, false, true>, dp, k, out_map);
-    else if (t.stream_b) e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true, true>, dp, k, out_map);
-    else e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false, true>, dp, k, out_map);
+    if (fused && t.stream_b) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true, true>, dp, k, out_map, a_map)
+                                      : cudaLaunchKernelEx(&cfg, k_tc<true, float, true, true>, dp, k, out_map, a_map);
+    else if (fused) e = bf16 ? cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false, true>, dp, k, out_map, a_map)
+                             : cudaLaunchKernelEx(&cfg, k_tc<true, float, false, true>, dp, k, out_map, a_map);
+    else if (t.stream_b) e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true, true>, dp, k, out_map, a_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false, true>, dp, k, out_map, a_map);
   } else if (fused && t.stream_b) {
-    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true>, dp, k, out_map);
-    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, true>, dp, k, out_map);
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, true>, dp, k, out_map, a_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, true>, dp, k, out_map, a_map);
   } else if (fused) {
-    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false>, dp, k, out_map);
-    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, false>, dp, k, out_map);
+    if (bf16) e = cudaLaunchKernelEx(&cfg, k_tc<true, uint16_t, false>, dp, k, out_map, a_map);
+    else e = cudaLaunchKernelEx(&cfg, k_tc<true, float, false>, dp, k, out_map, a_map);
   } else if (t.stream_b) {
-    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true>, dp, k, out_map);
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, true>, dp, k, out_map, a_map);
   } else {
-    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false>, dp, k, out_map);
+    e = cudaLaunchKernelEx(&cfg, k_tc<false, float, false>, dp, k, out_map, a_map);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_msg = cudaGetErrorString(e); return ITLUMM_ECUDA; }

@@ -93,3 +93,59 @@ def test_packed_rows_register_tree_walk_paths(seed, N, D, M, C, dtype):
     got = np.stack([(c[:, i // 2] >> (4 * (i % 2))) & 15 for i in range(C)], axis=1)
     assert np.array_equal(got, ref["codes"])
     assert np.array_equal(y.cpu().numpy().view(np.uint32), ref["y"].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,N,D,M,C,dtype,pad", [(41, 1, 64, 40, 8, "f32", 0), (42, 129, 200, 300, 20, "f32", 0),
+                                                    (43, 1000, 500, 520, 33, "f32", 8), (44, 700, 300, 96, 12, "bf16", 0),
+                                                    (45, 300, 50, 64, 4, "f32", 0)])
+def test_fused_tc_on_packed_rows(seed, N, D, M, C, dtype, pad):
+    """The fused tensor-core kernel on split-packed rows: f32 rows staged K-block by K-block by TMA
+    into the one-hot stage and overwritten in place (C >= 8; ragged last K-block C = 20, 33; a row
+    tail N = 129; two and three M slices; lda > 4C), bf16 and C < 8 on per-thread vector loads;
+    bit-exact against the oracle on whole rows, alone and through AUTO."""
+    torch = pytest.importorskip("torch")
+    from paper_2207_05808_b200 import Plan, split_packed
+    w, params = _case(seed, N, D, M, C, dtype)
+    pp, cols = split_packed(params)
+    ref = oracle.amm(params, w["A"], relu=w["relu"], dtype=dtype, nthreads=8)
+    Ap = np.ascontiguousarray(w["A"][:, cols])
+    if pad:
+        Ap = np.concatenate([Ap, np.full((N, pad), np.nan, Ap.dtype)], axis=1)
+    A = torch.from_numpy(Ap.view(np.int16) if dtype == "bf16" else Ap).cuda()
+    if dtype == "bf16":
+        A = A.view(torch.bfloat16)
+    if pad:
+        A = A[:, : 4 * C]
+    plan = Plan(pp, device=0)
+    for algo in ("tc", "auto"):
+        plan.set_algo(algo)
+        y = plan.amm(A, relu=w["relu"])
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy().view(np.uint32), ref["y"].view(np.uint32)), algo
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["tc", "auto"])
+def test_fused_tc_packed_cfg2_full_size_sampled(algo):
+    """BASELINE configs[1] split-packed at full size (N = 60000, 469 row tiles, 2 M slices): the
+    fused kernel (TMA-staged rows) against encode -> accumulate for every row and the oracle on whole
+    rows for sampled rows (tile and item-round boundaries, first and last rows)."""
+    torch = pytest.importorskip("torch")
+    from paper_2207_05808_b200 import Plan, split_packed
+    w = synth.workload("cfg2")
+    params = ofit.fit(w["A_train"], w["B"], w["C"], w["perm"], w["bias"])
+    pp, cols = split_packed(params)
+    plan = Plan(pp, device=0)
+    A = torch.from_numpy(np.ascontiguousarray(w["A"][:, cols])).cuda()
+    plan.set_algo("tc_pipe")
+    y_pipe = plan.amm(A, relu=True)
+    plan.set_algo(algo)
+    y = plan.amm(A, relu=True)
+    torch.cuda.synchronize()
+    y, y_pipe = y.cpu().numpy(), y_pipe.cpu().numpy()
+    assert np.array_equal(y.view(np.uint32), y_pipe.view(np.uint32))
+    edges = np.array([0, 1, 127, 128, 255, 256, 9471, 9472, 18943, 18944, 59903, 59904, 59998, 59999])
+    rows = np.unique(np.concatenate([np.random.default_rng(1).choice(60000, 2048, replace=False), edges]))
+    ref = oracle.amm(params, w["A"][rows], relu=True, nthreads=8)
+    assert np.array_equal(y[rows].view(np.uint32), ref["y"].view(np.uint32))

@@ -25,7 +25,11 @@ else:
     w = synth.workload(name, n_rows=cfg["N"])
 bf16 = cfg["dtype"] == "bf16"
 p = fit_layer(w["A_train"], w["B"], w["C"], w["perm"], w["bias"], a_is_bf16=bf16)
-plan = Plan(p, algo="tc" if mode == "acc" else "tc_pipe")
+if mode == "fusedpk":                                    # fused TC on split-packed rows
+    from paper_2207_05808_b200 import split_packed
+    p, cols = split_packed(p)
+    w["A"] = np.ascontiguousarray(w["A"][:, cols])
+plan = Plan(p, algo="tc" if mode in ("acc", "fusedpk") else "tc_pipe")
 A = torch.from_numpy(w["A"].view(np.int16) if bf16 else w["A"]).cuda()
 if bf16:
     A = A.view(torch.bfloat16)
