@@ -157,50 +157,10 @@ __host__ __device__ constexpr uint32_t idesc_i8_m256(int n) {
   return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
-// The streamlined dense producer (SS == 2 K-blocks per slot, KB even, codes straight from global
-// memory).  The generic loop below costs ~95 SASS instructions per thread and K-block (runtime SS
-// and tail handling, developer switches, address arithmetic): with three producer warps per SM
-// sub-partition that is ~0.4 us of issue per ring slot, the "bare ring" cost of DESIGN.md 7.1.
-// Here a K-block is ~45 instructions:
-//   * no validity handling: rows >= N are never stored (the TMA store clips them, the acc path
-//     checks the row) and codebooks >= C meet LUT rows that the plan zero-fills (tc_layout_host),
-//     so any nibble there adds 0;
-//   * the swizzle moves from the addresses to the data: thread (r, half) owns the 64-byte half
-//     (4 half) ^ (r & 4) of row r and writes its chunks at +0, +16, +32, +48; chunk j' holds
-//     codebook 4 half + (j' ^ (r & 3)), i.e. the nibble at bit (4 j') ^ (4 (r & 3)) of its 16 bits;
-//   * codes in batches of two 16-byte quads (8 K-blocks = 4 slots), the next batch loaded one batch
-//     ahead: fence.proxy.async compiles to MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC and the membar waits
-//     for an outstanding global load, so fewer, larger loads mean fewer stalled fences.
-// TAB: the 16-byte one-hot patterns come from a 16-entry shared-memory table (LDS.128) instead of
-// the shift arithmetic.
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-template <bool TAB>
-__device__ __forceinline__ void tcp_onehot_kblock(uint32_t addr, uint32_t word, uint32_t hs, const uint32_t (&cs)[4], uint32_t tab) {
-  if (TAB) {
-    const uint32_t v = (word >> hs) << 4;               // nibble i of the thread's 16 bits at bit 4 i + 4
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint32_t w0, w1, w2, w3;
-      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                   : "r"(tab + ((v >> cs[j]) & 0xF0u)));
-      sts128(addr + 16u * j, w0, w1, w2, w3);
-    }
-  } else {
-    const uint32_t v = (word >> hs) << 3;               // 8 * nibble i at bits 4 i + 3 .. 4 i + 6
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t sh = (v >> cs[j]) & 0x78u;         // 8 * code
-      sts128(addr + 16u * j, shl_clamp(1u, sh), shl_clamp(1u, sh - 32u), shl_clamp(1u, sh - 64u), shl_clamp(1u, sh - 96u));
-    }
-  }
-}
-
 // Per-CTA shared memory: ST ring slots of SS stages [A | metadata | B half], CS codes tiles (0: the
 // codes come straight from global memory), epilogue staging.
 struct TcpSmem {
-  size_t a_bytes, e_bytes, b_bytes, stage, ring, codes, stg, bar, tmem, tab, trc, total;
+  size_t a_bytes, e_bytes, b_bytes, stage, ring, codes, stg, bar, tmem, trc, total;
 };
 constexpr int kTcpTrcSlots = 24, kTcpTrcWin = 64, kTcpTrcFirst = 96;   // developer timeline window
 __host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int CS, int ldc, bool trace = false, int SS = 1) {
@@ -215,8 +175,7 @@ __host__ __device__ inline TcpSmem tcp_smem_layout(int mode, int NS, int ST, int
   s.stg = s.codes + (((size_t)CS * kTcRows * ldc + 1023) & ~(size_t)1023);
   s.bar = s.stg + (size_t)kTcEpiWarps * kTcStage;
   s.tmem = s.bar + (size_t)(2 * ST + 4 + 2 * CS) * 8;
-  s.tab = (s.tmem + 16 + 15) & ~(size_t)15;   // 16 one-hot patterns of 16 B (tcp_onehot_kblock<true>)
-  s.trc = s.tab + 256;
+  s.trc = s.tmem + 16;
   s.total = s.trc + (trace ? (size_t)kTcpTrcSlots * kTcpTrcWin * 8 : 0) + 1024;   // + slack for 1024-byte alignment
   return s;
 }
@@ -233,8 +192,6 @@ struct TcpKArgs {
   int pdl;
   uint64_t* trace;                     // developer timeline (ITLUMM_TC_TRACE=1): [4 CTAs][4 roles][kTraceEv]
   int cload;                           // codes tiles loaded by their own warp (16) instead of the LUT loader
-  int poll;                            // developer: barrier waits polled by lane 0 only (+ __syncwarp): 1 producers, 2 epilogue, 4 MMA warp
-  int fast;                            // streamlined dense producer loop (tcp_produce_dense): 1 ALU one-hot, 2 table
   int dbg;                             // developer removal switches (ITLUMM_TCP_DBG; results then wrong):
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
@@ -306,11 +263,6 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     for (int s = 0; s < CS; ++s) { mbar_init(codes_full + s, 1); mbar_init(codes_empty + s, kTcpProdWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (g.fast == 2 && warp == 1 && lane < 16) {
-    uint32_t w[4];
-    onehot_dense16((uint32_t)lane, w);
-    *reinterpret_cast<uint4*>(smem + L.tab + 16 * lane) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
   if (warp == kTcpLoaderWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qt_map)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&out_map)) : "memory");
@@ -325,14 +277,6 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
   cluster_sync_all();                                   // peer barriers initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  auto wait1 = [&](uint64_t* bar, uint32_t par, int bit) {   // wait, optionally polled by lane 0 only
-    if (g.poll & bit) {
-      if (lane == 0) mbar_wait(bar, par);
-      __syncwarp();
-    } else {
-      mbar_wait(bar, par);
-    }
-  };
   const uint32_t full_leader = mapa_shared(smem_u32(full_bar), 0);
   const uint32_t acce_leader = mapa_shared(smem_u32(acce_bar), 0);
   // plan memory only above; codes and out belong to the stream order
@@ -396,67 +340,8 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         }
       }
     }
-  } else if (role < kTcpProdWarps && g.fast) {
-    // ================================================================ producers, streamlined dense
-    // loop (see tcp_onehot_kblock): SS == 2, KB even, codes from global memory in two-quad batches
-    const int pt = role * 32 + lane;
-    const uint32_t r = (uint32_t)pt & (kTcRows - 1), half = (uint32_t)pt >> 7;
-    const uint32_t tbase = smem_u32(ring) + r * 128u + (((4u * half) ^ (r & 4u)) << 4);
-    const uint32_t rx = 4u * (r & 3u), hs = 16u * half;
-    const uint32_t cs4[4] = {rx, 4u ^ rx, 8u ^ rx, 12u ^ rx};
-    const uint32_t tab = smem_u32(smem + L.tab);
-    const uint32_t stage = (uint32_t)L.stage;
-    const bool use_tab = g.fast == 2;
-    const int nq = (KB + 3) >> 2;                        // 16-byte quads of codes per row
-    const int nbatch = (nq + 1) >> 1;
-    auto grow = [&](int64_t t) -> const uint8_t* {
-      const int64_t rw = t * 2 * kTcRows + (int64_t)rank * kTcRows + r;
-      return rw < g.N ? g.codes + rw * g.ldc : nullptr;
-    };
-    uint4 na = make_uint4(0, 0, 0, 0), nb = na;
-    auto loadb = [&](const uint8_t* row, int q0) {
-      if (row) {
-        na = __ldg(reinterpret_cast<const uint4*>(row) + q0);
-        if (q0 + 1 < nq) nb = __ldg(reinterpret_cast<const uint4*>(row) + q0 + 1);
-      }
-    };
-    int st = 0;
-    uint32_t ph = 0;
-    int64_t tile;
-    int sl;
-    if (item(0, tile, sl)) loadb(grow(tile), 0);
-    for (int64_t k = 0; item(k, tile, sl); ++k) {
-      const uint8_t* crow = grow(tile);
-      const uint8_t* cnext = nullptr;
-      {
-        int64_t t2;
-        int s2;
-        if (item(k + 1, t2, s2)) cnext = grow(t2);
-      }
-      for (int b = 0; b < nbatch; ++b) {
-        const uint32_t w[8] = {na.x, na.y, na.z, na.w, nb.x, nb.y, nb.z, nb.w};
-        if (b + 1 < nbatch) loadb(crow, 2 * (b + 1)); else loadb(cnext, 0);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (8 * b + 2 * s >= KB) break;
-          wait1(empty_bar + st, ph ^ 1, 1);
-          const uint32_t a0 = tbase + (uint32_t)(2 * st) * stage;
-          if (use_tab) {
-            tcp_onehot_kblock<true>(a0, w[2 * s], hs, cs4, tab);
-            tcp_onehot_kblock<true>(a0 + stage, w[2 * s + 1], hs, cs4, tab);
-          } else {
-            tcp_onehot_kblock<false>(a0, w[2 * s], hs, cs4, tab);
-            tcp_onehot_kblock<false>(a0 + stage, w[2 * s + 1], hs, cs4, tab);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(full_leader + 8u * st);
-          if (++st == ST) { st = 0; ph ^= 1; }
-        }
-      }
-    }
   } else if (role < kTcpProdWarps) {
-    // ================================================================ producers: two threads per row (generic loop)
+    // ================================================================ producers: two threads per row
     // Thread (r, half) writes codebooks 4*half .. 4*half+3 of each 8-codebook K-block of row r.
     const int pt = role * 32 + lane;
     const int r = pt & (kTcRows - 1);
@@ -524,7 +409,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           uint32_t code[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) code[j] = j < nv ? (cw >> (4 * j)) & 15u : 16u;
-          if (jj == 0) wait1(empty_bar + st, ph ^ 1, 1);
+          if (jj == 0) mbar_wait(empty_bar + st, ph ^ 1);
 
           uint8_t* stg_a = ring + (size_t)(st * SS + jj) * L.stage;
           if (g.dbg & 1) {
@@ -615,7 +500,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
         for (int kb = 0; kb < KBS;) {
           const int st1 = st + 1 == ST ? 0 : st + 1;
           const uint32_t ph1 = st + 1 == ST ? ph ^ 1 : ph;
-          wait1(full_bar + st, ph, 4);
+          mbar_wait(full_bar + st, ph);
           // the next stage too if it is already full (one issue pass for both), never wait for it
           const bool two = !(g.dbg & 4096) &&
                            __shfl_sync(0xffffffffu, (int)(kb + 1 < KBS && mbar_test(full_bar + st1, ph1)), 0) != 0;
@@ -658,7 +543,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     int64_t tile;
     int sl;
     for (int64_t k = 0; item(k, tile, sl); ++k) {
-      wait1(accf_bar + acc, aph, 2);
+      mbar_wait(accf_bar + acc, aph);
       tc_fence_after();
 
       const int m0 = sl * NS;
@@ -825,10 +710,6 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
   k.dbg = dbg;
   static const int cl_env = getenv("ITLUMM_TCP_CLOAD") ? atoi(getenv("ITLUMM_TCP_CLOAD")) : 1;   // developer
   k.cload = cl_env;
-  static const int fast_env = getenv("ITLUMM_TCP_FAST") ? atoi(getenv("ITLUMM_TCP_FAST")) : 0;   // developer: 1 streamlined ALU one-hot, 2 table (both measured slower)
-  static const int poll_env = getenv("ITLUMM_TCP_POLL") ? atoi(getenv("ITLUMM_TCP_POLL")) : 0;   // developer
-  k.poll = poll_env;
-  k.fast = (t.mode == kTcpDense && CS == 0 && t.SS == 2 && t.KB % 2 == 0 && dbg == 0 && !tr) ? fast_env : 0;
   const int64_t units = ((a.N + 255) / 256) * t.G;
   const void* kfn = t.mode == kTcpSparse ? (const void*)k_tcp<kTcpSparse> : (const void*)k_tcp<kTcpDense>;
   cudaLaunchConfig_t cfg{};

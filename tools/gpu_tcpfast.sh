@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the ITLUMM_TCP_FAST / ITLUMM_TCP_POLL switches exist only in commit b39554f; removed afterwards)
 # k_tcp streamlined dense producer (ITLUMM_TCP_FAST 0 generic / 1 ALU one-hot / 2 table): parity of
 # the streamed-LUT shapes under each, then the accumulate at cfg5 / cfg3 (kbench, one box).
 O=gpurun_out/tcpfast

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the ITLUMM_TCP_FAST / ITLUMM_TCP_POLL switches exist only in commit b39554f; removed afterwards)
 # k_tcp: who polls the barriers (ITLUMM_TCP_POLL bits: 1 producers, 2 epilogue, 4 MMA warp poll with
 # lane 0 only) x producer loop (ITLUMM_TCP_FAST), accumulate only (kbench), one box.
 O=gpurun_out/tcppoll
