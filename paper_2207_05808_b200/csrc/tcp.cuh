@@ -192,6 +192,7 @@ struct TcpKArgs {
   int pdl;
   uint64_t* trace;                     // developer timeline (ITLUMM_TC_TRACE=1): [4 CTAs][4 roles][kTraceEv]
   int cload;                           // codes tiles loaded by their own warp (16) instead of the LUT loader
+  int out_hint;                        // L2 policy of the output tensor stores (l2_policy kind; chosen in tcp_launch)
   int dbg;                             // developer removal switches (ITLUMM_TCP_DBG; results then wrong):
                                        // 1 producers skip the one-hot stores, 2 no MMAs (commits only),
                                        // 4 no LUT loads, 8 producers skip fence.proxy.async,
@@ -539,6 +540,7 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
     uint8_t* stg = smem + L.stg + (size_t)e * kTcStage;
     int acc = 0;
     uint32_t aph = 0;
+    const uint64_t opol = l2_policy(g.out_hint);
     bool pending = false;
     int64_t tile;
     int sl;
@@ -592,7 +594,8 @@ k_tcp(DevPlan p, TcpKArgs g, const __grid_constant__ CUtensorMap out_map, const 
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && !(g.dbg & 16)) {
-            tma_store_2d(&out_map, stg, m0 + j0, (int)row0);
+            if (g.out_hint) tma_store_2d_hint(&out_map, stg, m0 + j0, (int)row0, opol);
+            else tma_store_2d(&out_map, stg, m0 + j0, (int)row0);
             bulk_commit();
           }
           pending = !(g.dbg & 16);
@@ -710,6 +713,13 @@ inline itlumm_status tcp_launch(const TcpPlan& t, const DevPlan& dp, const TcArg
   k.dbg = dbg;
   static const int cl_env = getenv("ITLUMM_TCP_CLOAD") ? atoi(getenv("ITLUMM_TCP_CLOAD")) : 1;   // developer
   k.cload = cl_env;
+  // Output stores carry L2 evict_first when the call's output is far larger than the L2 (> 1 GB: cfg5's
+  // 4.3 GB, cfg4's hidden layers), so that the stream does not push codes and LUT out: k_tcp 3.14 -> 3.09 ms
+  // at cfg5.  Smaller outputs keep the default policy: with the hint the row-major cfg3 step ran 154 -> 160
+  // us although both kernels alone were no slower (the write-back then competes with the next call's
+  // HBM-bound row encoder).  Developer override: ITLUMM_OUT_HINT (l2_policy kind).
+  static const int oh_env = getenv("ITLUMM_OUT_HINT") ? atoi(getenv("ITLUMM_OUT_HINT")) : -1;
+  k.out_hint = oh_env >= 0 ? oh_env : ((unsigned long long)a.N * (unsigned long long)dp.M * 4ull > (1ull << 30) ? 1 : 0);
   const int64_t units = ((a.N + 255) / 256) * t.G;
   const void* kfn = t.mode == kTcpSparse ? (const void*)k_tcp<kTcpSparse> : (const void*)k_tcp<kTcpDense>;
   cudaLaunchConfig_t cfg{};
